@@ -1,0 +1,189 @@
+/*
+ * chp_b200.h -- C ABI of the B200 (sm_100a) hot path of the convex-hull
+ * preconditioner (arXiv 1505.00914, Algorithm 1 + Lemma-1 compaction + hull).
+ *
+ * Plain C: POD arguments, device pointers are plain `int32_t*` etc., no torch
+ * or CUDA types in any signature (streams travel as `void*`).  Every call is
+ * stream-ordered on the context's stream; functions that return results to
+ * the host say so.  One context per device per host thread; contexts are not
+ * thread-safe, different contexts are independent.
+ *
+ * Status codes: CHP_OK; CHP_EINVAL where the reference throws
+ * std::invalid_argument; CHP_EDEVICE for CUDA failures (the C++ drop-in maps
+ * it to std::runtime_error).  chp_last_error() describes the last failure.
+ *
+ * Reference interfaces each entry point replaces (paths under
+ * /root/reference/proj):
+ *   chp_reduce            chp::reducer::reduce          include/chp/reducer.hpp:65-67,
+ *                                                       src/reducer.cpp:172-182 (+ bucket :122-135)
+ *   chp_compact           chp::reducer::build_polyline  include/chp/reducer.hpp:76, src/reducer.cpp:211-222;
+ *                         ExtremalArray::valid_count    src/reducer.cpp:145-152;
+ *                         occupancy::BlockedBitset words include/chp/occupancy.hpp:58-109;
+ *                         serialize's (width+1,-1) form  src/reducer.cpp:224-233
+ *   chp_ns_chain          the north_star chain order (no reference function)
+ *   chp_hull              chp::hulls::melkman           include/chp/hulls.hpp:24, src/hulls.cpp:396-440
+ *                         + canonicalize_hull           src/geometry.cpp:407-445
+ *   chp_bounds            chp::kernels::min_max         include/chp/kernels.hpp:33, src/kernels.cpp:580-583
+ *   chp_translate         chp::kernels::translate       include/chp/kernels.hpp:34-35, src/kernels.cpp:585-590
+ *   chp_pipeline_host     reduce + build_polyline (+ melkman) from HOST buffers, the drop-in's
+ *                         workhorse (src/reducer.cpp:172-182, :211-222; src/hulls.cpp:396-440)
+ *   chp_precondition_host chp::reducer::precondition    include/chp/reducer.hpp:100-101,
+ *                                                       src/reducer.cpp:235-281
+ */
+#ifndef CHP_B200_H
+#define CHP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CHP_OK 0
+#define CHP_EINVAL 1
+#define CHP_EDEVICE 2
+
+typedef struct chp_ctx chp_ctx;
+
+/* ---------------------------------------------------------------- context */
+int chp_ctx_create(int device, chp_ctx** out);
+void chp_ctx_destroy(chp_ctx* ctx);
+const char* chp_last_error(const chp_ctx* ctx);
+/* Run on a caller-owned cudaStream_t (e.g. torch's current stream); NULL is
+ * the legacy default stream.  chp_ctx_use_own_stream() switches back to the
+ * context's own non-blocking stream (the initial state). */
+int chp_ctx_set_stream(chp_ctx* ctx, void* cuda_stream);
+int chp_ctx_use_own_stream(chp_ctx* ctx);
+void* chp_ctx_stream(const chp_ctx* ctx);
+int chp_ctx_sync(chp_ctx* ctx);
+/* Number of kernels this context has launched (evidence for the bench). */
+uint64_t chp_launch_count(const chp_ctx* ctx);
+/* Kernel-variant name chosen by the last chp_reduce ("smem32", "smem16",
+ * "global", "filter"). */
+const char* chp_last_variant(const chp_ctx* ctx);
+
+/* ------------------------------------------------- device-form L ("DL")
+ * int32[chp_dl_len(width)] = width pairs (lo, ~hi), empty = (INT32_MAX,
+ * INT32_MAX), then the error word (0 ok, -1 = an out-of-range coordinate
+ * was seen), then one pad word.  Every word is min-combined, so partial DLs
+ * from several devices merge with one element-wise MIN all-reduce. */
+uint64_t chp_dl_len(int64_t width);
+
+/* ------------------------------------------------------- K1: reduction */
+#define CHP_REDUCE_ACCUMULATE 1u   /* do not initialise d_L first            */
+#define CHP_REDUCE_NO_VALIDATE 2u  /* precondition path: y is not checked    */
+#define CHP_REDUCE_FORCE_GLOBAL 4u /* testing: force the global-L variant    */
+#define CHP_REDUCE_FORCE_SMEM32 8u /* testing: force 8-byte smem slots       */
+#define CHP_REDUCE_FORCE_FILTER 16u /* testing: force the smem-filter variant */
+
+/* Algorithm 1 over n int32 (x,y) pairs at d_xy (8-byte aligned).  Slot of a
+ * point is x - x_off - 1; a point is valid when that slot is in [0,width)
+ * and (unless NO_VALIDATE) 1 <= y <= q (q < 0: no upper bound).  Invalid
+ * points are skipped and flagged in d_L's error word; chp_check() turns the
+ * flag into CHP_EINVAL.  Asynchronous. */
+int chp_reduce(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t width,
+               int64_t q, int64_t x_off, int32_t* d_L, uint32_t flags);
+
+/* Initialise d_L to all-empty / no-error.  Asynchronous. */
+int chp_dl_init(chp_ctx* ctx, int32_t* d_L, int64_t width);
+
+/* Rebuild a DL from (lo,hi) pairs in serialize form (empty = any lo > hi,
+ * e.g. the (width+1,-1) sentinel).  Used when a caller hands back a host
+ * ExtremalArray (build_polyline on an array it built or edited).  Async. */
+int chp_dl_from_pairs(chp_ctx* ctx, const int32_t* d_Lpairs, int64_t width,
+                      int32_t* d_L);
+
+/* Synchronise and read d_L's error word: CHP_EINVAL if an invalid
+ * coordinate was seen (reference: std::invalid_argument,
+ * src/reducer.cpp:175-178). */
+int chp_check(chp_ctx* ctx, const int32_t* d_L, int64_t width);
+
+/* ------------------------------------------------------ K3: compaction
+ * Single-pass decoupled-look-back scan over the slots of d_L.  All output
+ * pointers are optional (NULL = not produced):
+ *   d_chain  : int32 (x,y)[<= 2*width]  Lemma-1 order: per valid slot
+ *              ascending, to_original(i,lo) then to_original(i,hi) if hi!=lo
+ *   d_occ    : uint64[ceil(width/64)]   BlockedBitset<uint64_t> words
+ *   d_Lpairs : int32 (lo,hi)[width]     empty slots as (width+1,-1)
+ *   d_lower  : int32 (major,lo+minor_off)[v]  valid slots ascending
+ *   d_upper  : int32 (major,hi+minor_off)[v]  valid slots ascending
+ *   d_upperd : int32 (major,hi+minor_off)[s-v] slots with hi!=lo ascending
+ * d_counts (required, int64[4]) receives {s, v, err, s-v}: chain length
+ * (= valid_count), valid slots, the error word, two-point slots.  The
+ * mapping is ExtremalArray::to_original (include/chp/reducer.hpp:46-50):
+ * original = (slot + major_off, value + minor_off), axes swapped back when
+ * `swapped`.  width <= 2^29.  Asynchronous. */
+int chp_compact(chp_ctx* ctx, const int32_t* d_L, int64_t width,
+                int64_t major_off, int64_t minor_off, int swapped,
+                int32_t* d_chain, uint64_t* d_occ, int32_t* d_Lpairs,
+                int32_t* d_lower, int32_t* d_upper, int32_t* d_upperd,
+                int64_t* d_counts);
+
+/* The north_star order from chp_compact's d_lower/d_upperd/d_counts: minima
+ * by increasing x, then maxima (hi != lo only) by decreasing x.  d_ns has
+ * room for 2*width points.  Asynchronous. */
+int chp_ns_chain(chp_ctx* ctx, const int32_t* d_lower, const int32_t* d_upperd,
+                 const int64_t* d_counts, int64_t width, int32_t* d_ns);
+
+/* ------------------------------------------------------------- K4: hull
+ * Exact strict convex hull of the reduced set from chp_compact's
+ * d_lower / d_upper / d_counts, canonical like canonicalize_hull: CCW,
+ * starting at the lexicographically smallest vertex, 1 or 2 vertices when
+ * degenerate.  d_hull has room for 2*width+2 points; *d_h receives h
+ * (device int64).  `swapped` as in chp_compact.  Asynchronous. */
+int chp_hull(chp_ctx* ctx, const int32_t* d_lower, const int32_t* d_upper,
+             const int64_t* d_counts, int64_t width, int swapped,
+             int32_t* d_hull, int64_t* d_h);
+
+/* --------------------------------------------------- K0: bounds/translate */
+/* out4 (device int32[4]) = {x_min, x_max, y_min, y_max}; n >= 1. */
+int chp_bounds(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int32_t* d_out4);
+/* out[i] = in[i] + (dx, dy); in and out may alias. */
+int chp_translate(chp_ctx* ctx, const int32_t* d_in, uint64_t n, int32_t dx,
+                  int32_t dy, int32_t* d_out);
+
+/* ------------------------------------------------ host-buffer pipelines
+ * Inputs and outputs in HOST memory; pinned inputs are copied directly,
+ * pageable ones through the context's pinned staging.  The copy of chunk
+ * k+1 overlaps the reduction of chunk k.  All outputs optional; synchronous;
+ * CHP_EINVAL on an out-of-range coordinate (reduce) or an empty chain when a
+ * chain / hull was requested (build_polyline, melkman). */
+int chp_pipeline_host(chp_ctx* ctx, const int32_t* h_xy, uint64_t n,
+                      int64_t width, int64_t q, int32_t* h_Lpairs,
+                      uint64_t* h_occ, int32_t* h_chain, int64_t* h_s,
+                      int32_t* h_hull, int64_t* h_h);
+
+/* build_polyline / valid_count of a HOST L in serialize form (h_Lpairs,
+ * empty slots any lo > hi) with ExtremalArray's offsets: uploads L, K3 on
+ * device, chain back.  h_chain holds 2*width points.  CHP_EINVAL when no
+ * slot is valid and h_chain is requested (src/reducer.cpp:219-220). */
+int chp_polyline_host(chp_ctx* ctx, const int32_t* h_Lpairs, int64_t width,
+                      int64_t major_off, int64_t minor_off, int swapped,
+                      int32_t* h_chain, int64_t* h_s);
+
+/* precondition (x-only mode, src/reducer.cpp:235-281): bounds, width =
+ * x_max-x_min+1, fold with x_off = x_min-1 and y untranslated, Lemma-1
+ * chain.  h_bbox4 = {x_min,x_max,y_min,y_max}.  The chain buffer must hold
+ * 2*width points: call with h_chain == NULL first to learn width via
+ * h_bbox4.  n >= 1 (else CHP_EINVAL). */
+int chp_precondition_host(chp_ctx* ctx, const int32_t* h_xy, uint64_t n,
+                          int64_t* h_bbox4, int32_t* h_Lpairs, int32_t* h_chain,
+                          int64_t* h_s, int32_t* h_hull, int64_t* h_h);
+
+/* ------------------------------------------------- synthetic workloads
+ * Deterministic, counter-based generators of the BASELINE.json configs
+ * (DESIGN.md "Workloads"); identical bytes on host and device.  config:
+ * 2 Gaussian, 3 disk, 4 clusters, 5 hot columns (point i of the stream is
+ * a pure function of (config, seed, p, offset+i)).  Config 1 is the
+ * reference's own sequential uniform-box generator (std::mt19937_64,
+ * src/dataset.cpp:35-59) and exists on the host only. */
+int chp_generate(chp_ctx* ctx, int config, uint64_t seed, int64_t p,
+                 uint64_t offset, uint64_t n, int32_t* d_xy);
+int chp_generate_host(int config, uint64_t seed, int64_t p, uint64_t offset,
+                      uint64_t n, int32_t* h_xy, int threads);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CHP_B200_H */

@@ -1,0 +1,316 @@
+// abi.cu -- context management and the host-buffer pipelines of the C ABI.
+//
+// chp_pipeline_host is what the C++ drop-in (reducer::reduce,
+// build_polyline, hulls::melkman) and the end-to-end bench call: the input
+// is streamed to the device in chunks on a copy stream while K1 reduces the
+// previous chunk on the compute stream (two device buffers, event-ordered),
+// then K3 (+K4) run on device and only L / the chain / the hull come back.
+#include <algorithm>
+#include <cstring>
+
+#include "chp_internal.cuh"
+
+namespace {
+
+constexpr uint64_t kChunkPts = 16ull << 20;  // 16 Mi points = 128 MiB per chunk
+
+void free_buf(DevBuf& b) {
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.bytes = 0;
+}
+
+bool is_pinned(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+// Streams h_xy[0..n) to the device in chunks and enqueues launch(d, m) on
+// the compute stream for each chunk as soon as its copy has landed.
+template <typename Launch>
+int stream_chunks(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, Launch&& launch) {
+    if (n == 0) return CHP_OK;
+    const bool pinned = is_pinned(h_xy);
+    const uint64_t chunk = std::min<uint64_t>(kChunkPts, n);
+    const size_t bytes = (size_t)chunk * 8;
+    int rc;
+    for (int b = 0; b < 2; ++b)
+        if ((rc = chp_ensure(ctx, ctx->stage_dev[b], bytes))) return rc;
+    if (!pinned && ctx->stage_bytes < bytes) {
+        for (int b = 0; b < 2; ++b) {
+            if (ctx->stage_host[b]) cudaFreeHost(ctx->stage_host[b]);
+            ctx->stage_host[b] = nullptr;
+        }
+        for (int b = 0; b < 2; ++b) CHP_CUDA(ctx, cudaMallocHost(&ctx->stage_host[b], bytes));
+        ctx->stage_bytes = bytes;
+    }
+    // The previous call may still be reading the staging buffers.
+    for (int b = 0; b < 2; ++b) {
+        CHP_CUDA(ctx, cudaEventRecord(ctx->ev_consumed[b], ctx->stream));
+        CHP_CUDA(ctx, cudaEventRecord(ctx->ev_copied[b], ctx->copy_stream));
+    }
+    uint64_t k = 0;
+    for (uint64_t off = 0; off < n; off += chunk, ++k) {
+        const int b = (int)(k & 1);
+        const uint64_t m = std::min<uint64_t>(chunk, n - off);
+        const int32_t* src = h_xy + 2 * off;
+        if (!pinned) {
+            // The previous H2D out of this staging buffer must have finished.
+            CHP_CUDA(ctx, cudaEventSynchronize(ctx->ev_copied[b]));
+            std::memcpy(ctx->stage_host[b], src, (size_t)m * 8);
+            src = (const int32_t*)ctx->stage_host[b];
+        }
+        CHP_CUDA(ctx, cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_consumed[b], 0));
+        CHP_CUDA(ctx, cudaMemcpyAsync(ctx->stage_dev[b].p, src, (size_t)m * 8, cudaMemcpyHostToDevice,
+                                      ctx->copy_stream));
+        CHP_CUDA(ctx, cudaEventRecord(ctx->ev_copied[b], ctx->copy_stream));
+        CHP_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_copied[b], 0));
+        if ((rc = launch((const int32_t*)ctx->stage_dev[b].p, m))) return rc;
+        CHP_CUDA(ctx, cudaEventRecord(ctx->ev_consumed[b], ctx->stream));
+    }
+    return CHP_OK;
+}
+
+// Streams h_xy[0..n) into ctx->dl (accumulating; it must be initialised).
+int stream_reduce(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t width, int64_t q, int64_t x_off,
+                  uint32_t flags) {
+    return stream_chunks(ctx, h_xy, n, [&](const int32_t* d, uint64_t m) {
+        return chp_reduce(ctx, d, m, width, q, x_off, (int32_t*)ctx->dl.p, flags | CHP_REDUCE_ACCUMULATE);
+    });
+}
+
+// Compaction (+ hull) of ctx->dl, then the requested outputs to the host.
+int finish_host(chp_ctx* ctx, int64_t width, int64_t major_off, int64_t minor_off, int32_t* h_Lpairs,
+                uint64_t* h_occ, int32_t* h_chain, int64_t* h_s, int32_t* h_hull, int64_t* h_h,
+                bool chain_required) {
+    int rc;
+    const size_t W = (size_t)width;
+    if ((rc = chp_ensure(ctx, ctx->counts, 16 * sizeof(int64_t)))) return rc;
+    if ((rc = chp_ensure(ctx, ctx->chain, 2 * W * 8))) return rc;
+    if ((rc = chp_ensure(ctx, ctx->occ, ((W + 63) / 64) * 8))) return rc;
+    if ((rc = chp_ensure(ctx, ctx->lpairs, W * 8))) return rc;
+    const bool want_hull = h_hull || h_h;
+    if (want_hull) {
+        if ((rc = chp_ensure(ctx, ctx->lower, W * 8))) return rc;
+        if ((rc = chp_ensure(ctx, ctx->upper, W * 8))) return rc;
+        if ((rc = chp_ensure(ctx, ctx->hull, (2 * W + 4) * 8))) return rc;
+    }
+    int64_t* d_counts = (int64_t*)ctx->counts.p;
+    if ((rc = chp_compact(ctx, (const int32_t*)ctx->dl.p, width, major_off, minor_off, 0,
+                          (h_chain || h_s) ? (int32_t*)ctx->chain.p : nullptr,
+                          h_occ ? (uint64_t*)ctx->occ.p : nullptr, h_Lpairs ? (int32_t*)ctx->lpairs.p : nullptr,
+                          want_hull ? (int32_t*)ctx->lower.p : nullptr,
+                          want_hull ? (int32_t*)ctx->upper.p : nullptr, nullptr, d_counts)))
+        return rc;
+    if (want_hull) {
+        if ((rc = chp_hull(ctx, (const int32_t*)ctx->lower.p, (const int32_t*)ctx->upper.p, d_counts, width, 0,
+                           (int32_t*)ctx->hull.p, d_counts + 4)))
+            return rc;
+    }
+    int64_t cnt[8];
+    CHP_CUDA(ctx, cudaMemcpyAsync(cnt, d_counts, sizeof cnt, cudaMemcpyDeviceToHost, ctx->stream));
+    CHP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    if (cnt[2] != 0) return chp_einval(ctx, "reduce: coordinate out of range");
+    const int64_t s = cnt[0];
+    if (h_s) *h_s = s;
+    if (s == 0 && chain_required) return chp_einval(ctx, "build_polyline: no valid points");
+    if (h_Lpairs)
+        CHP_CUDA(ctx, cudaMemcpyAsync(h_Lpairs, ctx->lpairs.p, W * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    if (h_occ)
+        CHP_CUDA(ctx, cudaMemcpyAsync(h_occ, ctx->occ.p, ((W + 63) / 64) * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    if (h_chain && s > 0)
+        CHP_CUDA(ctx, cudaMemcpyAsync(h_chain, ctx->chain.p, (size_t)s * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    if (want_hull) {
+        if (h_h) *h_h = cnt[4];
+        if (h_hull && cnt[4] > 0)
+            CHP_CUDA(ctx, cudaMemcpyAsync(h_hull, ctx->hull.p, (size_t)cnt[4] * 8, cudaMemcpyDeviceToHost,
+                                          ctx->stream));
+    }
+    CHP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return CHP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int chp_ctx_create(int device, chp_ctx** out) {
+    if (!out) return CHP_EINVAL;
+    *out = nullptr;
+    chp_ctx* ctx = new chp_ctx();
+    ctx->device = device;
+    cudaError_t e = cudaSetDevice(device);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking);
+    for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
+        e = cudaEventCreateWithFlags(&ctx->ev_copied[b], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_consumed[b], cudaEventDisableTiming);
+    }
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
+    if (e == cudaSuccess)
+        e = cudaDeviceGetAttribute(&ctx->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->l2_bytes, cudaDevAttrL2CacheSize, device);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        delete ctx;
+        return CHP_EDEVICE;
+    }
+    ctx->stream = ctx->own_stream;
+    *out = ctx;
+    return CHP_OK;
+}
+
+void chp_ctx_destroy(chp_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    cudaStreamSynchronize(ctx->copy_stream);
+    DevBuf* bufs[] = {&ctx->tile_status, &ctx->hull_a, &ctx->hull_b, &ctx->hull_cnt_a, &ctx->hull_cnt_b,
+                      &ctx->filter, &ctx->dl, &ctx->counts, &ctx->chain, &ctx->lower, &ctx->upper,
+                      &ctx->hull, &ctx->occ, &ctx->lpairs, &ctx->stage_dev[0], &ctx->stage_dev[1]};
+    for (DevBuf* b : bufs) free_buf(*b);
+    for (int b = 0; b < 2; ++b) {
+        if (ctx->stage_host[b]) cudaFreeHost(ctx->stage_host[b]);
+        if (ctx->ev_copied[b]) cudaEventDestroy(ctx->ev_copied[b]);
+        if (ctx->ev_consumed[b]) cudaEventDestroy(ctx->ev_consumed[b]);
+    }
+    if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+    delete ctx;
+}
+
+const char* chp_last_error(const chp_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int chp_ctx_set_stream(chp_ctx* ctx, void* stream) {
+    if (!ctx) return CHP_EINVAL;
+    ctx->stream = (cudaStream_t)stream;
+    return CHP_OK;
+}
+
+int chp_ctx_use_own_stream(chp_ctx* ctx) {
+    if (!ctx) return CHP_EINVAL;
+    ctx->stream = ctx->own_stream;
+    return CHP_OK;
+}
+
+void* chp_ctx_stream(const chp_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+int chp_ctx_sync(chp_ctx* ctx) {
+    if (!ctx) return CHP_EINVAL;
+    CHP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return CHP_OK;
+}
+
+uint64_t chp_launch_count(const chp_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+const char* chp_last_variant(const chp_ctx* ctx) { return ctx ? ctx->variant : "none"; }
+
+int chp_pipeline_host(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t width, int64_t q,
+                      int32_t* h_Lpairs, uint64_t* h_occ, int32_t* h_chain, int64_t* h_s, int32_t* h_hull,
+                      int64_t* h_h) {
+    if (!ctx) return CHP_EINVAL;
+    if (width < 1) return chp_einval(ctx, "reduce: width must be >= 1");
+    if (width > (1ll << 29)) return chp_einval(ctx, "reduce: width exceeds the device limit 2^29");
+    CHP_CUDA(ctx, cudaSetDevice(ctx->device));
+    int rc;
+    if ((rc = chp_ensure(ctx, ctx->dl, chp_dl_len(width) * 4))) return rc;
+    if ((rc = chp_dl_init(ctx, (int32_t*)ctx->dl.p, width))) return rc;
+    if ((rc = stream_reduce(ctx, h_xy, n, width, q, 0, 0))) return rc;
+    return finish_host(ctx, width, 0, 0, h_Lpairs, h_occ, h_chain, h_s, h_hull, h_h,
+                       h_chain != nullptr || h_hull != nullptr);
+}
+
+int chp_polyline_host(chp_ctx* ctx, const int32_t* h_Lpairs, int64_t width, int64_t major_off, int64_t minor_off,
+                      int swapped, int32_t* h_chain, int64_t* h_s) {
+    if (!ctx) return CHP_EINVAL;
+    if (width < 1 || width > (1ll << 29)) return chp_einval(ctx, "build_polyline: width must be in [1, 2^29]");
+    CHP_CUDA(ctx, cudaSetDevice(ctx->device));
+    int rc;
+    const size_t W = (size_t)width;
+    if ((rc = chp_ensure(ctx, ctx->lpairs, W * 8))) return rc;
+    if ((rc = chp_ensure(ctx, ctx->dl, chp_dl_len(width) * 4))) return rc;
+    if ((rc = chp_ensure(ctx, ctx->chain, 2 * W * 8))) return rc;
+    if ((rc = chp_ensure(ctx, ctx->counts, 16 * sizeof(int64_t)))) return rc;
+    CHP_CUDA(ctx, cudaMemcpyAsync(ctx->lpairs.p, h_Lpairs, W * 8, cudaMemcpyHostToDevice, ctx->stream));
+    if ((rc = chp_dl_from_pairs(ctx, (const int32_t*)ctx->lpairs.p, width, (int32_t*)ctx->dl.p))) return rc;
+    int64_t* d_counts = (int64_t*)ctx->counts.p;
+    if ((rc = chp_compact(ctx, (const int32_t*)ctx->dl.p, width, major_off, minor_off, swapped,
+                          (int32_t*)ctx->chain.p, nullptr, nullptr, nullptr, nullptr, nullptr, d_counts)))
+        return rc;
+    int64_t cnt[4];
+    CHP_CUDA(ctx, cudaMemcpyAsync(cnt, d_counts, sizeof cnt, cudaMemcpyDeviceToHost, ctx->stream));
+    CHP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    if (h_s) *h_s = cnt[0];
+    if (h_chain) {
+        if (cnt[0] == 0) return chp_einval(ctx, "build_polyline: no valid points");
+        CHP_CUDA(ctx, cudaMemcpy(h_chain, ctx->chain.p, (size_t)cnt[0] * 8, cudaMemcpyDeviceToHost));
+    }
+    return CHP_OK;
+}
+
+int chp_precondition_host(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t* h_bbox4, int32_t* h_Lpairs, int32_t* h_chain,
+                          int64_t* h_s, int32_t* h_hull, int64_t* h_h) {
+    if (!ctx) return CHP_EINVAL;
+    if (n == 0) return chp_einval(ctx, "precondition: empty input");
+    CHP_CUDA(ctx, cudaSetDevice(ctx->device));
+    // Step 1 (bounds).  The points stay resident for step 3 when they fit a
+    // quarter of free memory; otherwise they are streamed twice.
+    int rc;
+    size_t freeb = 0, totalb = 0;
+    CHP_CUDA(ctx, cudaMemGetInfo(&freeb, &totalb));
+    const bool resident = (size_t)n * 8 <= freeb / 4;
+    DevBuf pts;
+    if (resident) {
+        if ((rc = chp_ensure(ctx, pts, (size_t)n * 8))) return rc;
+        CHP_CUDA(ctx, cudaMemcpyAsync(pts.p, h_xy, (size_t)n * 8, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    if ((rc = chp_ensure(ctx, ctx->counts, 16 * sizeof(int64_t)))) return rc;
+    int32_t* d_b4 = (int32_t*)((int64_t*)ctx->counts.p + 8);
+    int32_t b4[4];
+    if (resident) {
+        if ((rc = chp_bounds(ctx, (const int32_t*)pts.p, n, d_b4))) return rc;
+        CHP_CUDA(ctx, cudaMemcpyAsync(b4, d_b4, 16, cudaMemcpyDeviceToHost, ctx->stream));
+        CHP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    } else {
+        if ((rc = chp_bounds_init(ctx, d_b4))) return rc;
+        if ((rc = stream_chunks(ctx, h_xy, n, [&](const int32_t* d, uint64_t m) {
+                 return chp_bounds_accumulate(ctx, d, m, d_b4);
+             })))
+            return rc;
+        CHP_CUDA(ctx, cudaMemcpyAsync(b4, d_b4, 16, cudaMemcpyDeviceToHost, ctx->stream));
+        CHP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    }
+    for (int i = 0; i < 4; ++i) h_bbox4[i] = b4[i];
+    const int64_t width = (int64_t)b4[1] - b4[0] + 1;
+    if (!h_chain && !h_hull && !h_s && !h_Lpairs) {
+        free_buf(pts);
+        return CHP_OK;
+    }
+    if (width > (1ll << 29)) {
+        free_buf(pts);
+        return chp_einval(ctx, "precondition: x extent exceeds the device limit 2^29");
+    }
+    const int64_t x_off = (int64_t)b4[0] - 1;  // major_offset, src/reducer.cpp:258
+    if ((rc = chp_ensure(ctx, ctx->dl, chp_dl_len(width) * 4))) return rc;
+    if (resident) {
+        rc = chp_reduce(ctx, (const int32_t*)pts.p, n, width, -1, x_off, (int32_t*)ctx->dl.p,
+                        CHP_REDUCE_NO_VALIDATE);
+    } else {
+        rc = chp_dl_init(ctx, (int32_t*)ctx->dl.p, width);
+        if (!rc) rc = stream_reduce(ctx, h_xy, n, width, -1, x_off, CHP_REDUCE_NO_VALIDATE);
+    }
+    if (rc) {
+        free_buf(pts);
+        return rc;
+    }
+    rc = finish_host(ctx, width, x_off, 0, h_Lpairs, nullptr, h_chain, h_s, h_hull, h_h, true);
+    cudaStreamSynchronize(ctx->stream);
+    free_buf(pts);
+    return rc;
+}
+
+}  // extern "C"

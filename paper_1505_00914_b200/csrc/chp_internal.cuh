@@ -1,0 +1,113 @@
+// chp_internal.cuh -- context, launch bookkeeping and device helpers shared
+// by the sm_100a kernels behind include/chp_b200.h.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include "chp_b200.h"
+
+#define CHP_EMPTY INT_MAX  // lo and ~hi of an empty slot
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+};
+
+struct chp_ctx {
+    int device = 0;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr;  // host pipeline: H2D overlapped with K1
+    int sm_count = 148;
+    int smem_optin = 227 * 1024;
+    int l2_bytes = 0;
+    uint64_t launches = 0;
+    std::string err;
+    const char* variant = "none";
+    // scratch owned by the context
+    DevBuf tile_status;  // K3 decoupled look-back status words
+    DevBuf hull_a, hull_b, hull_cnt_a, hull_cnt_b;
+    DevBuf filter;       // K1 filter snapshot
+    DevBuf dl;           // host pipeline: device-form L
+    DevBuf counts;       // host pipeline: int64[8]
+    DevBuf chain, lower, upper, hull, occ, lpairs;
+    DevBuf stage_dev[2]; // host pipeline: device input chunks
+    void* stage_host[2] = {nullptr, nullptr};  // pinned staging for pageable inputs
+    size_t stage_bytes = 0;
+    cudaEvent_t ev_copied[2] = {nullptr, nullptr};
+    cudaEvent_t ev_consumed[2] = {nullptr, nullptr};
+};
+
+// Record the first CUDA error of a launch sequence in ctx->err.
+static inline int chp_cuda_fail(chp_ctx* ctx, cudaError_t e, const char* what) {
+    ctx->err = std::string(what) + ": " + cudaGetErrorString(e);
+    return CHP_EDEVICE;
+}
+#define CHP_CUDA(ctx, call)                                                 \
+    do {                                                                    \
+        cudaError_t e_ = (call);                                            \
+        if (e_ != cudaSuccess) return chp_cuda_fail((ctx), e_, #call);      \
+    } while (0)
+#define CHP_LAUNCHED(ctx)                                                   \
+    do {                                                                    \
+        (ctx)->launches++;                                                  \
+        cudaError_t e_ = cudaGetLastError();                                \
+        if (e_ != cudaSuccess) return chp_cuda_fail((ctx), e_, "kernel launch"); \
+    } while (0)
+
+static inline int chp_einval(chp_ctx* ctx, const char* msg) {
+    ctx->err = msg;
+    return CHP_EINVAL;
+}
+
+// Grow-only device scratch.
+static inline int chp_ensure(chp_ctx* ctx, DevBuf& b, size_t bytes) {
+    if (b.bytes >= bytes) return CHP_OK;
+    if (b.p) {
+        cudaStreamSynchronize(ctx->stream);
+        cudaFree(b.p);
+        b.p = nullptr;
+        b.bytes = 0;
+    }
+    size_t want = bytes < 256 ? 256 : bytes;
+    CHP_CUDA(ctx, cudaMalloc(&b.p, want));
+    b.bytes = want;
+    return CHP_OK;
+}
+
+// K0 pieces used by the host pipelines (misc.cu).
+int chp_bounds_init(chp_ctx* ctx, int32_t* d_out4);
+int chp_bounds_accumulate(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int32_t* d_out4);
+
+// ----------------------------------------------------------- device side
+
+// 128-bit streaming load: read-only path, no L1 allocation, 256-byte L2
+// sector prefetch (the point stream is touched exactly once, sequentially).
+__device__ __forceinline__ int4 ld_stream(const int4* p) {
+    int4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.s32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+// L2-coherent load of a slot pair that other CTAs update atomically.
+__device__ __forceinline__ int2 ld_cg2(const int2* p) {
+    int2 r;
+    asm volatile("ld.global.cg.v2.s32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+    return r;
+}
+// Fire-and-forget global min (SASS RED.MIN).
+__device__ __forceinline__ void red_min(int* p, int v) {
+    asm volatile("red.relaxed.gpu.global.min.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Slot of x for offset x_off, as an unsigned value that is < width exactly
+// when x - x_off - 1 is in [0, width).  Computed mod 2^32 (x_off + 1 fits
+// int32 whenever a valid point exists).
+__device__ __forceinline__ uint32_t slot_of(int32_t x, uint32_t base) {
+    return (uint32_t)x - base;
+}

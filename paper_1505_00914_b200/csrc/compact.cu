@@ -1,0 +1,228 @@
+// compact.cu -- K3: skip-invalid compaction of L into the ordered chain.
+//
+// Replaces build_polyline (/root/reference/proj/src/reducer.cpp:211-222),
+// the ctz walk of the occupancy words it iterates
+// (include/chp/occupancy.hpp:83-93), ExtremalArray::valid_count
+// (src/reducer.cpp:145-152) and serialize's (width+1,-1) form (:224-233).
+//
+// One pass over the 8-byte slots with a single-pass decoupled look-back scan
+// (tiles of 2048 slots, 256 threads x 8 slots, dynamic tile order so every
+// predecessor of a tile has started).  The scanned value packs two counters
+// in a u64: c = 1 + [hi != lo] per valid slot (chain positions, Lemma-1
+// order) in the low word and v = [valid] (lower/upper positions) in the high
+// word.  Status words carry a 2-bit flag and both counters in 31 bits each,
+// hence width <= 2^29.  A warp of 8-slot masks is folded into 64-bit
+// occupancy words with three shuffles (the paper's bit array M, in
+// BlockedBitset<uint64_t> layout).
+#include <algorithm>
+
+#include "chp_internal.cuh"
+
+namespace {
+
+constexpr int kCT = 256;      // threads per tile
+constexpr int kItems = 8;      // slots per thread
+constexpr int kTile = kCT * kItems;
+
+constexpr unsigned long long kFlagAgg = 1ull << 62;
+constexpr unsigned long long kFlagIncl = 2ull << 62;
+constexpr unsigned long long kMask31 = (1ull << 31) - 1;
+
+__device__ __forceinline__ unsigned long long pack_status(unsigned long long flag, unsigned long long cv) {
+    return flag | (cv & kMask31) | (((cv >> 32) & kMask31) << 31);
+}
+__device__ __forceinline__ unsigned long long unpack_cv(unsigned long long st) {
+    return (st & kMask31) | (((st >> 31) & kMask31) << 32);
+}
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+struct Map {
+    long long major_off, minor_off;
+    int swapped;
+};
+__device__ __forceinline__ int2 to_original(const Map& m, long long slot1, long long value) {
+    const int32_t major = (int32_t)(slot1 + m.major_off);
+    const int32_t minor = (int32_t)(value + m.minor_off);
+    return m.swapped ? make_int2(minor, major) : make_int2(major, minor);
+}
+
+__global__ void __launch_bounds__(kCT) k_compact(const int* __restrict__ DL, uint32_t width, Map map,
+                                                 int2* __restrict__ chain, unsigned long long* __restrict__ occ,
+                                                 int2* __restrict__ lpairs, int2* __restrict__ lower,
+                                                 int2* __restrict__ upper, int2* __restrict__ upperd,
+                                                 long long* __restrict__ counts,
+                                                 unsigned long long* __restrict__ status, uint32_t ntiles) {
+    __shared__ uint32_t s_tile;
+    __shared__ unsigned long long s_warp[kCT / 32];
+    __shared__ unsigned long long s_excl;
+    unsigned int* tile_counter = reinterpret_cast<unsigned int*>(status + ntiles);
+    if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t slot0 = (uint64_t)tile * kTile + (uint64_t)threadIdx.x * kItems;
+    const int2* gL = reinterpret_cast<const int2*>(DL);
+
+    int lo[kItems], hi[kItems];
+    uint32_t vmask = 0, dmask = 0;
+#pragma unroll
+    for (int j = 0; j < kItems; ++j) {
+        const uint64_t s = slot0 + j;
+        lo[j] = CHP_EMPTY;
+        hi[j] = INT_MIN;
+        if (s < width) {
+            const int2 e = gL[s];
+            lo[j] = e.x;
+            hi[j] = ~e.y;
+        }
+        if (lo[j] <= hi[j]) {
+            vmask |= 1u << j;
+            if (lo[j] != hi[j]) dmask |= 1u << j;
+        }
+    }
+    const uint32_t nv = __popc(vmask), nd = __popc(dmask);
+    const unsigned long long mine = (unsigned long long)(nv + nd) | ((unsigned long long)nv << 32);
+
+    // Block exclusive scan of `mine`.
+    unsigned long long incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        unsigned long long w = lane < kCT / 32 ? s_warp[lane] : 0ull;
+#pragma unroll
+        for (int o = 1; o < kCT / 32; o <<= 1) {
+            const unsigned long long t = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += t;
+        }
+        if (lane < kCT / 32) s_warp[lane] = w;  // inclusive warp prefix
+    }
+    __syncthreads();
+    const unsigned long long warp_excl = warp ? s_warp[warp - 1] : 0ull;
+    const unsigned long long tile_agg = s_warp[kCT / 32 - 1];
+    const unsigned long long thread_excl = warp_excl + incl - mine;
+
+    // Decoupled look-back (warp 0).
+    if (warp == 0) {
+        unsigned long long excl = 0;
+        if (tile == 0) {
+            if (lane == 0) st_release(status + tile, pack_status(kFlagIncl, tile_agg));
+        } else {
+            if (lane == 0) st_release(status + tile, pack_status(kFlagAgg, tile_agg));
+            long long pred = (long long)tile - 1;
+            for (;;) {
+                const long long t = pred - lane;
+                unsigned long long st = t >= 0 ? ld_acquire(status + t) : kFlagIncl;
+                while (__any_sync(0xffffffffu, (st >> 62) == 0)) {
+                    if ((st >> 62) == 0) st = ld_acquire(status + t);
+                }
+                const unsigned incl_lanes = __ballot_sync(0xffffffffu, (st >> 62) == 2);
+                const int stop = incl_lanes ? __ffs(incl_lanes) - 1 : 31;
+                unsigned long long val = (lane <= stop) ? unpack_cv(st) : 0ull;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+                excl += val;
+                if (incl_lanes) break;
+                pred -= 32;
+            }
+            if (lane == 0) st_release(status + tile, pack_status(kFlagIncl, excl + tile_agg));
+        }
+        if (lane == 0) s_excl = excl;
+    }
+    __syncthreads();
+    const unsigned long long pre = s_excl + thread_excl;
+    uint32_t C = (uint32_t)pre;          // chain position (Lemma-1 order)
+    uint32_t V = (uint32_t)(pre >> 32);  // valid-slot position
+
+#pragma unroll
+    for (int j = 0; j < kItems; ++j) {
+        const uint64_t s = slot0 + j;
+        if (s >= width) break;
+        const bool v = (vmask >> j) & 1, d = (dmask >> j) & 1;
+        if (lpairs) lpairs[s] = v ? make_int2(lo[j], hi[j]) : make_int2((int)(width + 1), -1);
+        if (!v) continue;
+        const long long slot1 = (long long)s + 1;
+        if (chain) {
+            chain[C] = to_original(map, slot1, lo[j]);
+            if (d) chain[C + 1] = to_original(map, slot1, hi[j]);
+        }
+        const int32_t major = (int32_t)(slot1 + map.major_off);
+        if (lower) lower[V] = make_int2(major, (int32_t)(lo[j] + map.minor_off));
+        if (upper) upper[V] = make_int2(major, (int32_t)(hi[j] + map.minor_off));
+        if (upperd && d) upperd[C - V] = make_int2(major, (int32_t)(hi[j] + map.minor_off));
+        C += d ? 2 : 1;
+        V += 1;
+    }
+    if (occ) {
+        // 8 lanes x 8 slots = one 64-bit word (slot0 of lane 8k is 64-aligned).
+        unsigned long long word = (unsigned long long)vmask << (8 * (lane & 7));
+        word |= __shfl_xor_sync(0xffffffffu, word, 1);
+        word |= __shfl_xor_sync(0xffffffffu, word, 2);
+        word |= __shfl_xor_sync(0xffffffffu, word, 4);
+        const uint64_t wi = slot0 >> 6;
+        if ((lane & 7) == 0 && wi * 64 < width) occ[wi] = word;
+    }
+    if (tile == ntiles - 1 && threadIdx.x == kCT - 1) {
+        // The last tile's last thread holds the totals.
+        counts[0] = (long long)C;
+        counts[1] = (long long)V;
+        counts[2] = (long long)DL[2ull * width];
+        counts[3] = (long long)(C - V);
+    }
+}
+
+__global__ void k_ns_chain(const int2* __restrict__ lower, const int2* __restrict__ upperd,
+                           const long long* __restrict__ counts, uint64_t cap, int2* __restrict__ ns) {
+    const long long s = counts[0], v = counts[1], d = counts[3];
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < cap && (long long)k < s; k += stride)
+        ns[k] = (long long)k < v ? lower[k] : upperd[d - 1 - ((long long)k - v)];
+}
+
+}  // namespace
+
+extern "C" int chp_compact(chp_ctx* ctx, const int32_t* d_L, int64_t width, int64_t major_off,
+                           int64_t minor_off, int swapped, int32_t* d_chain, uint64_t* d_occ,
+                           int32_t* d_Lpairs, int32_t* d_lower, int32_t* d_upper, int32_t* d_upperd,
+                           int64_t* d_counts) {
+    if (!ctx) return CHP_EINVAL;
+    if (width < 1 || width > (1ll << 29)) return chp_einval(ctx, "compact: width must be in [1, 2^29]");
+    if (!d_counts) return chp_einval(ctx, "compact: counts buffer required");
+    const uint32_t ntiles = (uint32_t)((width + kTile - 1) / kTile);
+    int rc = chp_ensure(ctx, ctx->tile_status, (size_t)ntiles * 8 + 16);
+    if (rc) return rc;
+    CHP_CUDA(ctx, cudaMemsetAsync(ctx->tile_status.p, 0, (size_t)ntiles * 8 + 16, ctx->stream));
+    Map m{major_off, minor_off, swapped};
+    k_compact<<<ntiles, kCT, 0, ctx->stream>>>(
+        d_L, (uint32_t)width, m, reinterpret_cast<int2*>(d_chain), reinterpret_cast<unsigned long long*>(d_occ),
+        reinterpret_cast<int2*>(d_Lpairs), reinterpret_cast<int2*>(d_lower), reinterpret_cast<int2*>(d_upper),
+        reinterpret_cast<int2*>(d_upperd), reinterpret_cast<long long*>(d_counts),
+        reinterpret_cast<unsigned long long*>(ctx->tile_status.p), ntiles);
+    CHP_LAUNCHED(ctx);
+    return CHP_OK;
+}
+
+extern "C" int chp_ns_chain(chp_ctx* ctx, const int32_t* d_lower, const int32_t* d_upperd,
+                            const int64_t* d_counts, int64_t width, int32_t* d_ns) {
+    if (!ctx) return CHP_EINVAL;
+    if (width < 1) return chp_einval(ctx, "ns_chain: width must be >= 1");
+    const uint64_t cap = 2ull * (uint64_t)width;
+    const int blocks = (int)std::min<uint64_t>((cap + 255) / 256, (uint64_t)ctx->sm_count * 16);
+    k_ns_chain<<<blocks, 256, 0, ctx->stream>>>(reinterpret_cast<const int2*>(d_lower),
+                                                reinterpret_cast<const int2*>(d_upperd),
+                                                reinterpret_cast<const long long*>(d_counts), cap,
+                                                reinterpret_cast<int2*>(d_ns));
+    CHP_LAUNCHED(ctx);
+    return CHP_OK;
+}

@@ -1,0 +1,210 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle.
+
+Bit-exact for L (serialize form), the occupancy words, the Lemma-1 chain,
+s = valid_count, the north_star chain and the canonical hull, for every K1
+variant, on downscaled BASELINE.json configs, the reference's config-1
+golden digests, edge cases (empty, odd n, unaligned
+buffers, invalid coordinates) and randomized fixtures shaped like the
+reference's (tests/test_util.hpp).
+"""
+import numpy as np
+import pytest
+import torch
+
+from paper_1505_00914_b200 import _lib
+from paper_1505_00914_b200.device import generate_host
+
+from _cases import mixed_case, to_unit_box
+
+pytestmark = pytest.mark.gpu
+
+VARIANTS = {
+    "auto": 0,
+    "global": _lib.REDUCE_FORCE_GLOBAL,
+    "smem32": _lib.REDUCE_FORCE_SMEM32,
+    "filter": _lib.REDUCE_FORCE_FILTER,
+}
+
+
+def run_device(ctx, xy_np, p, q, flags=0, offset_points=0):
+    """H2D, K1, K3 (all outputs), K4, D2H.  offset_points > 0 places the
+    input at an 8-byte (not 16-byte) aligned address."""
+    n = len(xy_np)
+    buf = torch.empty((n + offset_points, 2), dtype=torch.int32, device="cuda")
+    buf[offset_points:] = torch.from_numpy(np.ascontiguousarray(xy_np))
+    xy = buf[offset_points:]
+    DL = ctx.reduce(xy, p, q=q, flags=flags)
+    comp = ctx.compact(DL, p, chain=True, occ=True, lpairs=True, lower=True, upper=True, upperd=True)
+    hull = ctx.hull(comp, p)
+    ns = ctx.ns_chain(comp, p)
+    torch.cuda.synchronize()
+    c = comp["counts"].cpu().numpy()
+    s, v = int(c[0]), int(c[1])
+    h = int(hull["h"].item())
+    return {
+        "err": int(c[2]), "s": s, "v": v,
+        "L": comp["lpairs"].cpu().numpy(),
+        "occ": comp["occ"].cpu().numpy().view(np.uint64),
+        "chain": comp["chain"][:s].cpu().numpy(),
+        "ns": ns[:s].cpu().numpy(),
+        "hull": hull["hull"][:h].cpu().numpy(),
+    }
+
+
+def check_against_oracle(orc, got, xy, p, q):
+    arr = orc.reduce(xy, p, q)
+    assert got["err"] == 0
+    assert np.array_equal(got["L"], orc.L_pairs(arr)), "L mismatch"
+    assert np.array_equal(got["occ"], arr["occ"]), "occupancy words mismatch"
+    s = orc.valid_count(arr)
+    assert got["s"] == s
+    if s == 0:
+        return
+    chain = orc.build_polyline(arr)
+    assert np.array_equal(got["chain"], chain), "Lemma-1 chain mismatch"
+    assert np.array_equal(got["ns"], orc.ns_chain(arr)), "north_star chain mismatch"
+    assert np.array_equal(got["hull"], orc.melkman(chain)), "hull mismatch"
+
+
+DOWNSCALED = [  # (config, p, n)
+    (2, 65536, 3_000_000),
+    (2, 4096, 1_000_000),
+    (3, 16384, 3_000_000),
+    (4, 1 << 20, 3_000_000),
+    (4, 8192, 1_000_000),
+    (5, 256, 3_000_000),
+]
+
+
+@pytest.mark.parametrize("config,p,n", DOWNSCALED)
+@pytest.mark.parametrize("variant", sorted(VARIANTS))
+def test_downscaled_configs(ctx, orc, config, p, n, variant):
+    if variant == "smem32" and p * 8 > 200 * 1024:
+        pytest.skip("table does not fit shared memory")
+    xy = generate_host(config, config, p, n)
+    got = run_device(ctx, xy, p, p, VARIANTS[variant])
+    check_against_oracle(orc, got, xy, p, p)
+
+
+def test_device_generator_matches_host(ctx):
+    for config, p in ((2, 65536), (3, 16384), (4, 1 << 20), (5, 256)):
+        n, off = 1_000_003, 123_456_789
+        d = ctx.generate(config, config, p, n, offset=off).cpu().numpy()
+        h = generate_host(config, config, p, n, offset=off)
+        assert np.array_equal(d, h), f"config {config}: device and host generators disagree"
+
+
+def test_config1_golden_digests(ctx, orc):
+    """SURVEY.md Appendix A, produced by the reference itself."""
+    xy = orc.uniform_box(1_000_000, 4096, 1)
+    assert orc.fnv(xy) == "17239ebe0273b7d1"
+    for flags in VARIANTS.values():
+        got = run_device(ctx, xy, 4096, 4096, flags)
+        assert orc.fnv(got["L"]) == "b5b55891aaae7596"
+        assert got["s"] == 8192
+        assert orc.fnv(got["chain"]) == "27d9354c9f73a66e"
+        assert got["hull"].tolist() == [[1, 49], [2, 3], [15, 1], [4067, 1], [4093, 4], [4095, 7], [4096, 56],
+                                        [4096, 4092], [4093, 4096], [21, 4096], [3, 4091], [1, 4071]]
+
+
+@pytest.mark.parametrize("offset_points", [0, 1])
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 31, 1001])
+def test_alignment_and_ragged_sizes(ctx, orc, n, offset_points):
+    rng = np.random.default_rng(n)
+    xy = rng.integers(1, 41, size=(n, 2)).astype(np.int32)
+    for flags in VARIANTS.values():
+        got = run_device(ctx, xy, 40, None, flags, offset_points)
+        check_against_oracle(orc, got, xy, 40, None)
+
+
+def test_empty_input(ctx):
+    xy = np.empty((0, 2), np.int32)
+    got = run_device(ctx, xy, 5, None)
+    assert got["s"] == 0 and got["v"] == 0 and got["err"] == 0
+    assert got["L"].tolist() == [[6, -1]] * 5
+
+
+@pytest.mark.parametrize("bad", [(6, 1), (0, 1), (1, 0), (1, 6), (-2147483648, 3), (3, -2147483648)])
+def test_validation_flags_invalid_points(ctx, bad):
+    xy = np.array([[1, 1], [2, 2], bad, [3, 3]], np.int32)
+    d = torch.from_numpy(xy).cuda()
+    for flags in VARIANTS.values():
+        DL = ctx.reduce(d, 5, q=5, flags=flags)
+        with pytest.raises(ValueError):
+            ctx.check(DL, 5)
+
+
+def test_large_y_without_q(ctx, orc):
+    """No q: y may reach INT32_MAX (the ~y encoding keeps it exact)."""
+    xy = np.array([[1, 2147483647], [1, 1], [2, 2147483647], [3, 5], [3, 2147483646]], np.int32)
+    for flags in VARIANTS.values():
+        got = run_device(ctx, xy, 3, None, flags)
+        check_against_oracle(orc, got, xy, 3, None)
+
+
+def test_randomized_fixtures(ctx, orc):
+    rng = np.random.default_rng(2026)
+    for trial in range(300):
+        n = int(rng.integers(1, 400)) if trial % 50 else 20000
+        pts, p = to_unit_box(mixed_case(rng, n))
+        for flags in (0, _lib.REDUCE_FORCE_GLOBAL):
+            got = run_device(ctx, pts, p, None, flags)
+            check_against_oracle(orc, got, pts, p, None)
+
+
+def test_heavy_skew_single_column(ctx, orc):
+    """Every point in one column (maximum contention), and two-point columns."""
+    rng = np.random.default_rng(9)
+    n = 2_000_000
+    xy = np.stack([np.full(n, 7), rng.integers(1, 1 << 20, size=n)], axis=1).astype(np.int32)
+    for flags in VARIANTS.values():
+        got = run_device(ctx, xy, 1 << 10, 1 << 20, flags)
+        check_against_oracle(orc, got, xy, 1 << 10, 1 << 20)
+
+
+def test_full_size_config2_vs_oracle(ctx, orc):
+    """BASELINE.json config 2 at full size (n = 1e8) against the oracle."""
+    p, n = 65536, 100_000_000
+    d = ctx.generate(2, 2, p, n)
+    DL = ctx.reduce(d, p, q=p)
+    comp = ctx.compact(DL, p, chain=True, lpairs=True, lower=True, upper=True)
+    hull = ctx.hull(comp, p)
+    torch.cuda.synchronize()
+    xy = d.cpu().numpy()
+    del d
+    arr = orc.reduce(xy, p, p)
+    c = comp["counts"].cpu().numpy()
+    assert np.array_equal(comp["lpairs"].cpu().numpy(), orc.L_pairs(arr))
+    chain = orc.build_polyline(arr)
+    assert int(c[0]) == len(chain)
+    assert np.array_equal(comp["chain"][: int(c[0])].cpu().numpy(), chain)
+    h = int(hull["h"].item())
+    assert np.array_equal(hull["hull"][:h].cpu().numpy(), orc.melkman(chain))
+
+
+@pytest.mark.parametrize("config", [3, 4, 5])
+def test_full_size_properties(ctx, config):
+    """Full BASELINE sizes (1e9 / 1e9 / 4e9 points): size-independent
+    properties.  (1) every K1 variant yields the same L; (2) sharding the
+    input and MIN-merging partial DLs (the multi-GPU combine) equals the
+    one-shot L; (3) idempotence: reducing the chain reproduces L;
+    (4) s <= 2p."""
+    import bench
+
+    n, p, seed, _ = bench.CONFIGS[config]
+    free = torch.cuda.mem_get_info()[0]
+    if n * 8 > free * 0.8:
+        pytest.skip("not enough device memory")
+    d = ctx.generate(config, seed, p, n)
+    ref_dl = ctx.reduce(d, p, q=p).clone()
+    for flags in (_lib.REDUCE_FORCE_GLOBAL, _lib.REDUCE_FORCE_FILTER):
+        assert torch.equal(ctx.reduce(d, p, q=p, flags=flags), ref_dl)
+    half = n // 2
+    a = ctx.reduce(d[:half], p, q=p).clone()
+    b = ctx.reduce(d[half:], p, q=p)
+    assert torch.equal(torch.minimum(a, b), ref_dl)
+    comp = ctx.compact(ref_dl, p, chain=True, lpairs=True)
+    s = int(comp["counts"][0].item())
+    assert 0 < s <= 2 * p
+    again = ctx.reduce(comp["chain"][:s].contiguous(), p, q=p)
+    assert torch.equal(again, ref_dl)
