@@ -75,7 +75,15 @@ uint64_t chp_dl_len(int64_t width);
 #define CHP_REDUCE_NO_VALIDATE 2u  /* precondition path: y is not checked    */
 #define CHP_REDUCE_FORCE_GLOBAL 4u /* testing: force the global-L variant    */
 #define CHP_REDUCE_FORCE_SMEM32 8u /* testing: force 8-byte smem slots       */
-#define CHP_REDUCE_FORCE_FILTER 16u /* testing: force the smem-filter variant */
+#define CHP_REDUCE_FORCE_FILTER 16u /* testing: force the column-group filter  */
+#define CHP_REDUCE_FORCE_FILTER8 32u /* testing: force the per-column filter   */
+#define CHP_REDUCE_FORCE_SMEM16 64u /* testing: force 4-byte packed smem slots */
+#define CHP_REDUCE_MISS_RED 128u    /* tuning: filter misses RED without reading */
+#define CHP_REDUCE_MISS_READ 256u   /* tuning: filter misses read the slot first */
+#define CHP_REDUCE_FILTER16 512u    /* tuning: 16-bit filter halves (default 8) */
+#define CHP_REDUCE_FILTER_SMALL 1024u /* tuning: filter table <= 100 KB (default 200 KB) */
+#define CHP_REDUCE_NO_TMA 2048u     /* tuning: stream via registers, not the TMA ring */
+#define CHP_REDUCE_TMA 4096u        /* tuning: stream via the TMA bulk-copy ring */
 
 /* Algorithm 1 over n int32 (x,y) pairs at d_xy (8-byte aligned).  Slot of a
  * point is x - x_off - 1; a point is valid when that slot is in [0,width)

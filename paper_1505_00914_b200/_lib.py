@@ -17,6 +17,8 @@ REDUCE_NO_VALIDATE = 2
 REDUCE_FORCE_GLOBAL = 4
 REDUCE_FORCE_SMEM32 = 8
 REDUCE_FORCE_FILTER = 16
+REDUCE_FORCE_FILTER8 = 32
+REDUCE_FORCE_SMEM16 = 64
 
 _lib = None
 

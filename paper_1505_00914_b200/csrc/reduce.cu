@@ -30,10 +30,11 @@
 #include <algorithm>
 
 #include "chp_internal.cuh"
+#include "stream.cuh"
 
 namespace {
 
-constexpr int kThreads = 512;
+constexpr int kThreads = 1024;
 
 struct Geo {
     uint32_t base;    // x_off + 1 (mod 2^32): slot = x - base
@@ -69,23 +70,43 @@ __device__ __forceinline__ void flag_error(bool bad, int* DL, uint32_t width) {
     if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) red_min(DL + 2ull * width, -1);
 }
 
-// Streams the points assigned to this thread (grid-stride over vectors,
-// unrolled 4x) and calls f(x, y) per point.
-template <typename F>
-__device__ __forceinline__ void for_each_point(const int32_t* __restrict__ xy, uint64_t n, F&& f) {
+// Streams the points assigned to this thread (grid-stride over 16-byte
+// vectors, 4 vectors per group) and calls f(x, y) per point.  Software
+// pipelined: the 4 loads of group k+1 are issued before group k is
+// processed, so 8 x 16 B per thread are in flight while the table is
+// updated and DRAM latency overlaps the per-point work.
+template <typename G, typename F>
+__device__ __forceinline__ void for_each_group(const int32_t* __restrict__ xy, uint64_t n, G&& g8, F&& f) {
     const Split sp = split_points(xy, n);
     const int4* __restrict__ v = reinterpret_cast<const int4*>(xy + 2 * sp.head);
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    for (; i + 3 * stride < sp.nvec; i += 4 * stride) {
-        const int4 a = ld_stream(v + i);
-        const int4 b = ld_stream(v + i + stride);
-        const int4 c = ld_stream(v + i + 2 * stride);
-        const int4 d = ld_stream(v + i + 3 * stride);
-        f(a.x, a.y); f(a.z, a.w);
-        f(b.x, b.y); f(b.z, b.w);
-        f(c.x, c.y); f(c.z, c.w);
-        f(d.x, d.y); f(d.z, d.w);
+    // Trip counts are warp-uniform (tested on the warp's last lane), so the
+    // full-mask __syncwarp below is always matched.
+    const uint64_t last = 31 - (threadIdx.x & 31);
+    if (i + last + 3 * stride < sp.nvec) {
+        int4 a = ld_stream(v + i), b = ld_stream(v + i + stride);
+        int4 c = ld_stream(v + i + 2 * stride), d = ld_stream(v + i + 3 * stride);
+        for (;;) {
+            const uint64_t nx = i + 4 * stride;
+            const bool more = nx + last + 3 * stride < sp.nvec;
+            int4 a2, b2, c2, d2;
+            if (more) {
+                a2 = ld_stream(v + nx);
+                b2 = ld_stream(v + nx + stride);
+                c2 = ld_stream(v + nx + 2 * stride);
+                d2 = ld_stream(v + nx + 3 * stride);
+            }
+            g8(a, b, c, d);
+            // Reconverge: a lane that took an update path (CAS loop, L2
+            // miss) must not leave the warp split for the rest of the
+            // stream, or every later load and compare is issued once per
+            // lane group (ncu: 13.7x instructions, 5.5x DRAM re-reads).
+            __syncwarp();
+            i = nx;
+            if (!more) break;
+            a = a2; b = b2; c = c2; d = d2;
+        }
     }
     for (; i < sp.nvec; i += stride) {
         const int4 a = ld_stream(v + i);
@@ -96,6 +117,96 @@ __device__ __forceinline__ void for_each_point(const int32_t* __restrict__ xy, u
         if (sp.tail) f(xy[2 * (n - 1)], xy[2 * (n - 1) + 1]);
     }
 }
+
+// Per-point form: the 8 points of a group are processed one after another.
+template <typename F>
+__device__ __forceinline__ void for_each_point(const int32_t* __restrict__ xy, uint64_t n, F&& f) {
+    for_each_group(
+        xy, n,
+        [&](const int4& a, const int4& b, const int4& c, const int4& d) {
+            f(a.x, a.y); f(a.z, a.w);
+            f(b.x, b.y); f(b.z, b.w);
+            f(c.x, c.y); f(c.z, c.w);
+            f(d.x, d.y); f(d.z, d.w);
+        },
+        f);
+}
+
+// Batched L2 path for the points of a group that the on-chip table could
+// not settle (bit k of `miss`): all their slot loads are issued before any
+// compare, so a thread waits for one L2 round trip per group instead of one
+// per miss.  READ_FIRST = false skips the loads and REDs both extremes
+// (fire-and-forget; right when most misses are real updates).
+template <bool READ_FIRST, int N>
+__device__ __forceinline__ void settle_misses(uint32_t miss, const uint32_t (&s)[N], const int (&y)[N],
+                                              int* __restrict__ DL) {
+    if (!miss) return;
+    const int2* gL = reinterpret_cast<const int2*>(DL);
+    if (READ_FIRST) {
+        int2 e[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k)
+            if ((miss >> k) & 1) e[k] = ld_cg2(gL + s[k]);
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+            if (!((miss >> k) & 1)) continue;
+            if (y[k] < e[k].x) red_min(DL + 2ull * s[k], y[k]);
+            if (~y[k] < e[k].y) red_min(DL + 2ull * s[k] + 1, ~y[k]);
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+            if (!((miss >> k) & 1)) continue;
+            red_min(DL + 2ull * s[k], y[k]);
+            red_min(DL + 2ull * s[k] + 1, ~y[k]);
+        }
+    }
+}
+
+__device__ __forceinline__ void unpack4(const int4& a, const int4& b, int (&x)[4], int (&y)[4]) {
+    x[0] = a.x; y[0] = a.y; x[1] = a.z; y[1] = a.w;
+    x[2] = b.x; y[2] = b.y; x[3] = b.z; y[3] = b.w;
+}
+
+// The point stream of one kernel: TMA ring (TMA = true; `ring` points at the
+// ring's shared memory) or software-pipelined registers.  g4(a, b) gets four
+// points at a time, f(x, y) single points (remainders).
+template <bool TMA, typename G4, typename F>
+__device__ __forceinline__ void stream_points(const int32_t* __restrict__ xy, uint64_t n, uint8_t* ring,
+                                              int stages, G4&& g4, F&& f) {
+    if (TMA) {
+        const Split sp = split_points(xy, n);
+        const int4* v = reinterpret_cast<const int4*>(xy + 2 * sp.head);
+        chpstream::tma_stream(v, sp.nvec, chpstream::ring_at(ring, stages), g4, [&](const int4& a) {
+            f(a.x, a.y);
+            f(a.z, a.w);
+        });
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            if (sp.head) f(xy[0], xy[1]);
+            if (sp.tail) f(xy[2 * (n - 1)], xy[2 * (n - 1) + 1]);
+        }
+    } else {
+        for_each_group(
+            xy, n,
+            [&](const int4& a, const int4& b, const int4& c, const int4& d) {
+                g4(a, b);
+                g4(c, d);
+            },
+            f);
+    }
+}
+
+// Four calls of a per-point functor.
+template <typename F>
+__device__ __forceinline__ auto per_point4(F& f) {
+    return [&f](const int4& a, const int4& b) {
+        f(a.x, a.y); f(a.z, a.w);
+        f(b.x, b.y); f(b.z, b.w);
+    };
+}
+
+// Dynamic shared memory: [table, 128-byte aligned][TMA ring].
+__host__ __device__ constexpr size_t table_span(size_t table_bytes) { return (table_bytes + 127) & ~(size_t)127; }
 
 // ------------------------------------------------------------- DL init
 __global__ void k_dl_init(int4* __restrict__ DL4, uint64_t nwords4, int* __restrict__ DL, uint32_t width) {
@@ -110,14 +221,17 @@ __global__ void k_dl_init(int4* __restrict__ DL4, uint64_t nwords4, int* __restr
 }
 
 // ------------------------------------------------------------ smem32
-template <bool VALIDATE>
+template <bool VALIDATE, bool TMA>
 __global__ void __launch_bounds__(kThreads) k_reduce_smem32(const int32_t* __restrict__ xy, uint64_t n,
-                                                            Geo g, uint32_t width, int* __restrict__ DL) {
-    extern __shared__ int2 sL[];
+                                                            Geo g, uint32_t width, int stages,
+                                                            int* __restrict__ DL) {
+    extern __shared__ uint4 smem4[];
+    int2* sL = reinterpret_cast<int2*>(smem4);
+    uint8_t* ring = reinterpret_cast<uint8_t*>(smem4) + table_span((size_t)width * 8);
     for (uint32_t c = threadIdx.x; c < width; c += blockDim.x) sL[c] = make_int2(CHP_EMPTY, CHP_EMPTY);
     __syncthreads();
     bool bad = false;
-    for_each_point(xy, n, [&](int32_t x, int32_t y) {
+    auto f = [&](int32_t x, int32_t y) {
         uint32_t s;
         if (!accept<VALIDATE>(g, x, y, s)) {
             bad = true;
@@ -126,7 +240,8 @@ __global__ void __launch_bounds__(kThreads) k_reduce_smem32(const int32_t* __res
         const int2 e = sL[s];
         if (y < e.x) atomicMin(&sL[s].x, y);
         if (~y < e.y) atomicMin(&sL[s].y, ~y);
-    });
+    };
+    stream_points<TMA>(xy, n, ring, stages, per_point4(f), f);
     flag_error(bad, DL, width);
     __syncthreads();
     // Flush: only slots where this CTA beats the current global value.
@@ -142,15 +257,17 @@ __global__ void __launch_bounds__(kThreads) k_reduce_smem32(const int32_t* __res
 
 // ------------------------------------------------------------ smem16
 // Slot word: bits 0-15 a = y - ybase (min), bits 16-31 b = 0xFFFF - a (min).
-template <bool VALIDATE>
+template <bool VALIDATE, bool TMA>
 __global__ void __launch_bounds__(kThreads) k_reduce_smem16(const int32_t* __restrict__ xy, uint64_t n,
-                                                            Geo g, uint32_t width, int32_t ybase,
+                                                            Geo g, uint32_t width, int32_t ybase, int stages,
                                                             int* __restrict__ DL) {
-    extern __shared__ uint32_t sW[];
+    extern __shared__ uint4 smem4[];
+    uint32_t* sW = reinterpret_cast<uint32_t*>(smem4);
+    uint8_t* ring = reinterpret_cast<uint8_t*>(smem4) + table_span((size_t)width * 4);
     for (uint32_t c = threadIdx.x; c < width; c += blockDim.x) sW[c] = 0xFFFFFFFFu;
     __syncthreads();
     bool bad = false;
-    for_each_point(xy, n, [&](int32_t x, int32_t y) {
+    auto f = [&](int32_t x, int32_t y) {
         uint32_t s;
         if (!accept<VALIDATE>(g, x, y, s)) {
             bad = true;
@@ -173,7 +290,8 @@ __global__ void __launch_bounds__(kThreads) k_reduce_smem16(const int32_t* __res
                 w = old;
             }
         }
-    });
+    };
+    stream_points<TMA>(xy, n, ring, stages, per_point4(f), f);
     flag_error(bad, DL, width);
     __syncthreads();
     int2* __restrict__ gL = reinterpret_cast<int2*>(DL);
@@ -190,12 +308,15 @@ __global__ void __launch_bounds__(kThreads) k_reduce_smem16(const int32_t* __res
 }
 
 // ------------------------------------------------------------ global
-template <bool VALIDATE>
+template <bool VALIDATE, bool TMA>
 __global__ void __launch_bounds__(kThreads) k_reduce_global(const int32_t* __restrict__ xy, uint64_t n,
-                                                            Geo g, uint32_t width, int* __restrict__ DL) {
+                                                            Geo g, uint32_t width, int stages,
+                                                            int* __restrict__ DL) {
+    extern __shared__ uint4 smem4[];
+    uint8_t* ring = reinterpret_cast<uint8_t*>(smem4);
     const int2* gL = reinterpret_cast<const int2*>(DL);
     bool bad = false;
-    for_each_point(xy, n, [&](int32_t x, int32_t y) {
+    auto one = [&](int32_t x, int32_t y) {
         uint32_t s;
         if (!accept<VALIDATE>(g, x, y, s)) {
             bad = true;
@@ -204,18 +325,43 @@ __global__ void __launch_bounds__(kThreads) k_reduce_global(const int32_t* __res
         const int2 e = ld_cg2(gL + s);
         if (y < e.x) red_min(DL + 2ull * s, y);
         if (~y < e.y) red_min(DL + 2ull * s + 1, ~y);
-    });
+    };
+    stream_points<TMA>(
+        xy, n, ring, stages,
+        [&](const int4& a, const int4& b) {
+            int x[4], y[4];
+            uint32_t s[4], miss = 0;
+            unpack4(a, b, x, y);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (accept<VALIDATE>(g, x[k], y[k], s[k]))
+                    miss |= 1u << k;
+                else
+                    bad = true;
+            }
+            settle_misses<true>(miss, s, y, DL);
+        },
+        one);
     flag_error(bad, DL, width);
 }
 
 // ------------------------------------------------------------ filter
-// Filter word per group of 2^gshift columns: bits 0-15 fa, 16-31 fb with
+// Filter word per group of 2^gshift columns, two H-bit halves (H = 8 in a
+// 16-bit word, or 16 in a 32-bit word): low half fa, high half fb with
 //   fa = ceil((max_lo - ybase) / 2^ys),  fb = floor((min_hi - ybase + 1) / 2^ys) - 1,
 // and a point is skipped iff fa <= u <= fb for u = (y - ybase) >> ys, which
 // implies max_lo <= y <= min_hi ("filter").  Empty / unusable
-// groups are 0x0000FFFF (fa = 0xFFFF > fb = 0).
+// groups are fa = all-ones, fb = 0 (never skip).
+template <typename W>
+struct FW {
+    static constexpr uint32_t kHalf = sizeof(W) * 4;
+    static constexpr uint32_t kMask = (1u << kHalf) - 1u;
+    static constexpr W kNever = (W)kMask;
+};
+
+template <typename W>
 __global__ void k_filter_build(const int* __restrict__ DL, uint32_t width, uint32_t gshift, int32_t ybase,
-                               uint32_t ys, uint32_t* __restrict__ F, uint32_t ngroups) {
+                               uint32_t ys, W* __restrict__ F, uint32_t ngroups) {
     const uint32_t gi = blockIdx.x * blockDim.x + threadIdx.x;
     if (gi >= ngroups) return;
     const int2* gL = reinterpret_cast<const int2*>(DL);
@@ -233,52 +379,202 @@ __global__ void k_filter_build(const int* __restrict__ DL, uint32_t width, uint3
         maxlo = lo > maxlo ? lo : maxlo;
         minhi = hi < minhi ? hi : minhi;
     }
-    uint32_t word = 0x0000FFFFu;
+    constexpr long long M = FW<W>::kMask;
+    W word = FW<W>::kNever;
     if (!empty && c0 < c1) {
         const long long q = 1ll << ys;
         long long a = maxlo - ybase;
         long long fa = a <= 0 ? 0 : (a + q - 1) / q;
         long long fb = (minhi - ybase + 1) >= 0 ? (minhi - ybase + 1) / q - 1 : -1;
-        if (fb > 0xFFFF) fb = 0xFFFF;
-        if (fa <= fb && fa <= 0xFFFF && fb >= 0) word = (uint32_t)fa | ((uint32_t)fb << 16);
+        if (fb > M) fb = M;
+        if (fa <= fb && fa <= M && fb >= 0) word = (W)((uint32_t)fa | ((uint32_t)fb << FW<W>::kHalf));
     }
     F[gi] = word;
 }
 
-template <bool VALIDATE>
+// F == nullptr starts from an all-"never skip" table (the warm-up pass:
+// every point is settled in L2, RED-only, building the first snapshot).
+template <typename W, bool VALIDATE, bool READ_FIRST, bool TMA>
 __global__ void __launch_bounds__(kThreads) k_reduce_filter(const int32_t* __restrict__ xy, uint64_t n,
                                                             Geo g, uint32_t width, uint32_t gshift,
                                                             int32_t ybase, uint32_t ys,
-                                                            const uint32_t* __restrict__ F, uint32_t ngroups,
+                                                            const W* __restrict__ F, uint32_t ngroups, int stages,
                                                             int* __restrict__ DL) {
-    extern __shared__ uint32_t sF[];
+    extern __shared__ uint4 sF4[];
+    W* sF = reinterpret_cast<W*>(sF4);
+    uint8_t* ring = reinterpret_cast<uint8_t*>(sF4) + table_span((size_t)ngroups * sizeof(W));
     {
-        const uint4* F4 = reinterpret_cast<const uint4*>(F);
-        uint4* s4 = reinterpret_cast<uint4*>(sF);
-        const uint32_t n4 = ngroups / 4;
-        for (uint32_t i = threadIdx.x; i < n4; i += blockDim.x) s4[i] = __ldcg(F4 + i);
-        for (uint32_t i = n4 * 4 + threadIdx.x; i < ngroups; i += blockDim.x) sF[i] = __ldcg(F + i);
+        const uint32_t per4 = 16 / sizeof(W);
+        const uint32_t n4 = ngroups / per4;
+        if (F) {
+            const uint4* F4 = reinterpret_cast<const uint4*>(F);
+            for (uint32_t i = threadIdx.x; i < n4; i += blockDim.x) sF4[i] = __ldcg(F4 + i);
+            for (uint32_t i = n4 * per4 + threadIdx.x; i < ngroups; i += blockDim.x) sF[i] = F[i];
+        } else {
+            for (uint32_t i = threadIdx.x; i < ngroups; i += blockDim.x) sF[i] = FW<W>::kNever;
+        }
     }
     __syncthreads();
-    const int2* gL = reinterpret_cast<const int2*>(DL);
+    constexpr uint32_t H = FW<W>::kHalf, HM = FW<W>::kMask;
+    const uint32_t ulim = HM << ys | ((1u << ys) - 1u);
+    // (uint32) y - ybase wraps for y < ybase; then it exceeds ulim and misses.
+    auto hit = [&](uint32_t s, int32_t y) {
+        const uint32_t w = sF[s >> gshift];
+        const uint32_t d = (uint32_t)y - (uint32_t)ybase;
+        const uint32_t u = d >> ys;
+        return d <= ulim && u >= (w & HM) && u <= (w >> H);
+    };
     bool bad = false;
-    for_each_point(xy, n, [&](int32_t x, int32_t y) {
+    auto one = [&](int32_t x, int32_t y) {
+        uint32_t s[1];
+        int yy[1] = {y};
+        if (!accept<VALIDATE>(g, x, y, s[0])) {
+            bad = true;
+            return;
+        }
+        settle_misses<true>(hit(s[0], y) ? 0u : 1u, s, yy, DL);
+    };
+    // RED-only misses are one-sided where the word allows: u <= fb means
+    // y <= min_hi of the group, so only lo can move; u >= fa means
+    // y >= max_lo, so only hi can move.
+    auto one_red = [&](int32_t x, int32_t y) {
         uint32_t s;
         if (!accept<VALIDATE>(g, x, y, s)) {
             bad = true;
             return;
         }
         const uint32_t w = sF[s >> gshift];
-        const uint32_t u = ((uint32_t)y - (uint32_t)ybase) >> ys;
-        // (uint32) y - ybase wraps for y < ybase; then u is huge and fails.
-        if ((uint32_t)y - (uint32_t)ybase <= (0xFFFFu << ys | ((1u << ys) - 1u)) && u >= (w & 0xFFFFu) &&
-            u <= (w >> 16))
-            return;
-        const int2 e = ld_cg2(gL + s);
-        if (y < e.x) red_min(DL + 2ull * s, y);
-        if (~y < e.y) red_min(DL + 2ull * s + 1, ~y);
-    });
+        const uint32_t d = (uint32_t)y - (uint32_t)ybase;
+        const uint32_t u = d >> ys;
+        const uint32_t fa = w & HM, fb = w >> H;
+        const bool in = d <= ulim;
+        const bool above_lo = in && u >= fa;  // y >= max_lo of the group
+        const bool below_hi = in && u <= fb;  // y <= min_hi of the group
+        if (above_lo && below_hi) return;
+        if (!above_lo) red_min(DL + 2ull * s, y);
+        if (!below_hi) red_min(DL + 2ull * s + 1, ~y);
+    };
+    if (READ_FIRST) {
+        stream_points<TMA>(
+            xy, n, ring, stages,
+            [&](const int4& a, const int4& b) {
+                int x[4], y[4];
+                uint32_t s[4], miss = 0;
+                unpack4(a, b, x, y);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    if (!accept<VALIDATE>(g, x[k], y[k], s[k]))
+                        bad = true;
+                    else if (!hit(s[k], y[k]))
+                        miss |= 1u << k;
+                }
+                settle_misses<true>(miss, s, y, DL);
+            },
+            one);
+    } else {
+        stream_points<TMA>(xy, n, ring, stages, per_point4(one_red), one_red);
+    }
     flag_error(bad, DL, width);
+}
+
+// ------------------------------------------------------------ filter8
+// Per-column learning filter for mid-size p (one 16-bit word per column:
+// bits 0-7 qa = ceil((lo-1) / 2^ys), bits 8-15 qb = floor(hi / 2^ys) - 1,
+// "never skip" = 0x00FF).  A point with u = (y-1) >> ys in [qa, qb] has
+// lo <= y <= hi for the column's current extremes and is skipped.  A miss
+// reads the column from L2 (ld.cg), REDs what it improves and writes the
+// tightened word back to shared memory, so each CTA's filter converges to
+// the global L as the pass proceeds.
+__device__ __forceinline__ uint16_t quant8(int lo, int hi, uint32_t ys) {
+    if (lo > hi || lo < 1) return 0x00FF;
+    const uint32_t a = ((uint32_t)(lo - 1) + ((1u << ys) - 1)) >> ys;
+    const int b = (int)((uint32_t)hi >> ys) - 1;
+    if (b < 0 || a > 255u || (int)a > b) return 0x00FF;
+    return (uint16_t)(a | ((uint32_t)min(b, 255) << 8));
+}
+
+__global__ void k_filter8_build(const int* __restrict__ DL, uint32_t width, uint32_t ys, uint16_t* __restrict__ F) {
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= width) return;
+    const int2 e = ld_cg2(reinterpret_cast<const int2*>(DL) + c);
+    F[c] = quant8(e.x, ~e.y, ys);
+}
+
+template <bool TMA>
+__global__ void __launch_bounds__(kThreads) k_reduce_filter8(const int32_t* __restrict__ xy, uint64_t n, Geo g,
+                                                             uint32_t width, uint32_t ys,
+                                                             const uint16_t* __restrict__ F, int stages,
+                                                             int* __restrict__ DL) {
+    extern __shared__ uint4 smem4[];
+    uint16_t* sF8 = reinterpret_cast<uint16_t*>(smem4);
+    uint8_t* ring = reinterpret_cast<uint8_t*>(smem4) + table_span((size_t)((width + 7) & ~7u) * 2);
+    {
+        const uint4* F4 = reinterpret_cast<const uint4*>(F);
+        uint4* s4 = reinterpret_cast<uint4*>(sF8);
+        const uint32_t n4 = width / 8;
+        for (uint32_t i = threadIdx.x; i < n4; i += blockDim.x) s4[i] = __ldcg(F4 + i);
+        for (uint32_t i = n4 * 8 + threadIdx.x; i < width; i += blockDim.x) sF8[i] = F[i];
+    }
+    __syncthreads();
+    // A word (qa <= qb) asserts lo <= qa*2^ys + 1 and hi >= (qb+1)*2^ys.  A
+    // point below that range can only lower lo, one above it only raise hi:
+    // one RED, then the word widens to include y (still true afterwards).
+    bool bad = false;
+    auto one = [&](int32_t x, int32_t y) {
+        uint32_t s;
+        if (!accept<true>(g, x, y, s)) {
+            bad = true;
+            return;
+        }
+        const uint32_t f = sF8[s];
+        const uint32_t qa = f & 0xFFu, qb = f >> 8;
+        const uint32_t u = ((uint32_t)y - 1u) >> ys;
+        if (u >= qa && u <= qb) return;
+        if (qa > qb) {  // nothing known: both extremes may move
+            red_min(DL + 2ull * s, y);
+            red_min(DL + 2ull * s + 1, ~y);
+            return;
+        }
+        if (u < qa) {
+            red_min(DL + 2ull * s, y);
+            sF8[s] = (uint16_t)((((uint32_t)(y - 1) + ((1u << ys) - 1)) >> ys) | (qb << 8));
+        } else {
+            red_min(DL + 2ull * s + 1, ~y);
+            sF8[s] = (uint16_t)(qa | (min(((uint32_t)y >> ys) - 1u, 255u) << 8));
+        }
+    };
+    stream_points<TMA>(xy, n, ring, stages, per_point4(one), one);
+    flag_error(bad, DL, width);
+}
+
+// Launch plan of one K1 kernel: table bytes in shared memory plus, when TMA
+// staging is on, a ring of as many 32 KB stages as fit (2..kMaxStages).
+// Per-variant defaults come from measurement ("K1 tuning"):
+// smem32 streams through the ring (its 128 KB table leaves one CTA/SM and
+// the ring restores the bytes in flight: C3 697 vs 673 Gpts/s); smem16 and
+// the filters stream through registers (C3 711 vs 568, C5 886 vs 702,
+// C2 417 vs 406).  CHP_REDUCE_TMA / CHP_REDUCE_NO_TMA override.
+constexpr int kMaxStages = 4;  // tools/micro_tma.cu: 4 x 32 KB beats 2 and 6
+
+struct Plan {
+    bool tma;
+    int stages;
+    size_t smem;
+};
+
+Plan plan_for(const chp_ctx* ctx, size_t table_bytes, uint32_t flags, bool tma_default) {
+    Plan p{false, 0, table_span(table_bytes)};
+    const bool want = (flags & CHP_REDUCE_TMA) ? true : (flags & CHP_REDUCE_NO_TMA) ? false : tma_default;
+    if (!want) return p;
+    const size_t limit = (size_t)ctx->smem_optin - 1024;
+    if (p.smem >= limit) return p;
+    int st = (int)((limit - p.smem) / chpstream::ring_bytes(1));
+    if (st > kMaxStages) st = kMaxStages;
+    if (st < 2) return p;
+    p.tma = true;
+    p.smem += chpstream::ring_bytes(st);
+    p.stages = st;
+    return p;
 }
 
 int blocks_for(chp_ctx* ctx, const void* fn, size_t smem, int cap_per_sm) {
@@ -287,6 +583,63 @@ int blocks_for(chp_ctx* ctx, const void* fn, size_t smem, int cap_per_sm) {
     if (per_sm < 1) per_sm = 1;
     if (per_sm > cap_per_sm) per_sm = cap_per_sm;
     return per_sm * ctx->sm_count;
+}
+
+// Launches kernel template K<..., TMA> with the plan's dynamic shared memory.
+#define CHP_LAUNCH_PLANNED(ctx, plan, KTMA, KREG, ...)                                                   \
+    do {                                                                                                 \
+        auto fn_ = (plan).tma ? (KTMA) : (KREG);                                                         \
+        CHP_CUDA((ctx), cudaFuncSetAttribute(fn_, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(plan).smem)); \
+        const int blocks_ = blocks_for((ctx), (const void*)fn_, (plan).smem, 2);                        \
+        fn_<<<blocks_, kThreads, (plan).smem, (ctx)->stream>>>(__VA_ARGS__);                            \
+        CHP_LAUNCHED(ctx);                                                                               \
+    } while (0)
+
+// Column-group snapshot filter in phases: a warm-up pass (n/64) through the
+// same kernel with an empty table (every point settled in L2, RED-only),
+// then snapshot -> n/8 -> snapshot -> the rest.  The table (W = 16-bit
+// words with 8-bit halves, or 32-bit words with 16-bit halves) is sized to
+// `fbudget` bytes; the rest of shared memory holds the TMA ring.
+template <typename W, bool V>
+int run_group_filter(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, const Geo& g, uint32_t w, int64_t q,
+                     uint32_t flags, size_t fbudget, int32_t* d_L) {
+    uint32_t ys = 0;
+    while ((uint64_t)(q - 1) >> ys > FW<W>::kMask) ++ys;
+    uint32_t gshift = 0;
+    while (((uint64_t)(w + (1u << gshift) - 1) >> gshift) * sizeof(W) > fbudget) ++gshift;
+    const uint32_t ngroups = (w + (1u << gshift) - 1) >> gshift;
+    int rc = chp_ensure(ctx, ctx->filter, (size_t)ngroups * sizeof(W) + 16);
+    if (rc) return rc;
+    const Plan pl = plan_for(ctx, (size_t)ngroups * sizeof(W), flags, false);
+    // Small groups: a miss is usually a real update -> RED directly.
+    // Wide groups: many misses are not -> read the slot first.
+    bool read_first = gshift >= 3;
+    if (flags & CHP_REDUCE_MISS_RED) read_first = false;
+    if (flags & CHP_REDUCE_MISS_READ) read_first = true;
+    const uint64_t warm = std::min<uint64_t>(n, n / 64) & ~1ull;
+    if (warm)
+        CHP_LAUNCH_PLANNED(ctx, pl, (k_reduce_filter<W, V, false, true>), (k_reduce_filter<W, V, false, false>), d_xy,
+                           warm, g, w, gshift, 1, ys, (const W*)nullptr, ngroups, pl.stages, d_L);
+    uint64_t done = warm;
+    const uint64_t bounds[2] = {std::min<uint64_t>(n, warm + n / 8) & ~1ull, n};
+    for (int ph = 0; ph < 2 && done < n; ++ph) {
+        k_filter_build<W><<<(ngroups + 255) / 256, 256, 0, ctx->stream>>>(d_L, w, gshift, 1, ys, (W*)ctx->filter.p,
+                                                                         ngroups);
+        CHP_LAUNCHED(ctx);
+        const uint64_t end = bounds[ph];
+        if (end > done) {
+            if (read_first)
+                CHP_LAUNCH_PLANNED(ctx, pl, (k_reduce_filter<W, V, true, true>), (k_reduce_filter<W, V, true, false>),
+                                   d_xy + 2 * done, end - done, g, w, gshift, 1, ys, (const W*)ctx->filter.p,
+                                   ngroups, pl.stages, d_L);
+            else
+                CHP_LAUNCH_PLANNED(ctx, pl, (k_reduce_filter<W, V, false, true>),
+                                   (k_reduce_filter<W, V, false, false>), d_xy + 2 * done, end - done, g, w, gshift,
+                                   1, ys, (const W*)ctx->filter.p, ngroups, pl.stages, d_L);
+            done = end;
+        }
+    }
+    return CHP_OK;
 }
 
 }  // namespace
@@ -305,8 +658,9 @@ extern "C" int chp_dl_init(chp_ctx* ctx, int32_t* d_L, int64_t width) {
     return CHP_OK;
 }
 
-// Choice of variant: the smallest smem footprint
-// that holds the exact table, else the filter path.
+// Choice of variant: the smallest shared-memory
+// footprint that holds the exact table (smem16, then smem32), else the
+// column-group filter when the y range is known, else the L2 table.
 extern "C" int chp_reduce(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t width, int64_t q,
                           int64_t x_off, int32_t* d_L, uint32_t flags) {
     if (!ctx) return CHP_EINVAL;
@@ -333,73 +687,94 @@ extern "C" int chp_reduce(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t
     const bool fits32 = (size_t)w * 8 <= budget;
     const bool y16 = validate && q >= 1 && q <= 65536;  // all valid y in [1, 65536]
     const bool fits16 = y16 && (size_t)w * 4 <= budget;
+    const bool yknown = validate && q >= 1;  // every accepted y is in [1, q]
+    const bool fits_f8 = yknown && (size_t)((w + 7) & ~7u) * 2 <= budget;
 
-    const bool force_global = flags & CHP_REDUCE_FORCE_GLOBAL;
-    const bool force_smem32 = flags & CHP_REDUCE_FORCE_SMEM32;
-    const bool force_filter = flags & CHP_REDUCE_FORCE_FILTER;
+    enum { V_GLOBAL, V_SMEM32, V_SMEM16, V_FILTER8, V_FILTER } v;
+    if (flags & CHP_REDUCE_FORCE_GLOBAL) v = V_GLOBAL;
+    else if ((flags & CHP_REDUCE_FORCE_SMEM32) && fits32) v = V_SMEM32;
+    else if ((flags & CHP_REDUCE_FORCE_SMEM16) && fits16) v = V_SMEM16;
+    else if ((flags & CHP_REDUCE_FORCE_FILTER8) && fits_f8) v = V_FILTER8;
+    else if ((flags & CHP_REDUCE_FORCE_FILTER) && yknown) v = V_FILTER;
+    else if (fits16) v = V_SMEM16;  // measured: 1.05-1.24x smem32 (C3, C5)
+    else if (fits32) v = V_SMEM32;
+    else if (yknown) v = V_FILTER;
+    else v = V_GLOBAL;
 
-    if (!force_global && !force_filter && (fits16 && !force_smem32)) {
-        const size_t smem = (size_t)w * 4;
-        auto fn = validate ? k_reduce_smem16<true> : k_reduce_smem16<false>;
-        CHP_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        const int cap = w >= 8192 ? 2 : 4;
-        const int blocks = blocks_for(ctx, (const void*)fn, smem, cap);
-        fn<<<blocks, kThreads, smem, ctx->stream>>>(d_xy, n, g, w, 1, d_L);
-        CHP_LAUNCHED(ctx);
-        ctx->variant = "smem16";
+    auto launch_global = [&](const int32_t* p, uint64_t m) -> int {
+        if (m == 0) return CHP_OK;
+        const Plan pl = plan_for(ctx, 0, flags, false);
+        if (validate)
+            CHP_LAUNCH_PLANNED(ctx, pl, (k_reduce_global<true, true>), (k_reduce_global<true, false>), p, m, g, w,
+                               pl.stages, d_L);
+        else
+            CHP_LAUNCH_PLANNED(ctx, pl, (k_reduce_global<false, true>), (k_reduce_global<false, false>), p, m, g, w,
+                               pl.stages, d_L);
         return CHP_OK;
-    }
-    if (!force_global && !force_filter && fits32) {
-        const size_t smem = (size_t)w * 8;
-        auto fn = validate ? k_reduce_smem32<true> : k_reduce_smem32<false>;
-        CHP_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        const int cap = w >= 8192 ? 2 : 4;
-        const int blocks = blocks_for(ctx, (const void*)fn, smem, cap);
-        fn<<<blocks, kThreads, smem, ctx->stream>>>(d_xy, n, g, w, d_L);
-        CHP_LAUNCHED(ctx);
-        ctx->variant = "smem32";
-        return CHP_OK;
-    }
-    if (force_filter || (!force_global && q >= 1)) {
-        // Filter path: warm-up prefix through L2, snapshot, filtered rest.
-        const int64_t yspan = q;  // valid y in [1, q]
-        uint32_t ys = 0;
-        while ((yspan - 1) >> ys > 0xFFFF) ++ys;
-        uint32_t gshift = 0;
-        while (((uint64_t)(w + (1u << gshift) - 1) >> gshift) * 4 > budget) ++gshift;
-        const uint32_t ngroups = (w + (1u << gshift) - 1) >> gshift;
-        int rc = chp_ensure(ctx, ctx->filter, (size_t)ngroups * 4 + 16);
-        if (rc) return rc;
-        const uint64_t warm = std::min<uint64_t>(n, std::max<uint64_t>(n / 64, (uint64_t)w * 4)) & ~1ull;
-        {
-            auto fn = validate ? k_reduce_global<true> : k_reduce_global<false>;
-            const int blocks = blocks_for(ctx, (const void*)fn, 0, 4);
-            if (warm > 0) {
-                fn<<<blocks, kThreads, 0, ctx->stream>>>(d_xy, warm, g, w, d_L);
-                CHP_LAUNCHED(ctx);
-            }
+    };
+
+    switch (v) {
+        case V_SMEM32: {
+            const Plan pl = plan_for(ctx, (size_t)w * 8, flags, true);
+            if (validate)
+                CHP_LAUNCH_PLANNED(ctx, pl, (k_reduce_smem32<true, true>), (k_reduce_smem32<true, false>), d_xy, n,
+                                   g, w, pl.stages, d_L);
+            else
+                CHP_LAUNCH_PLANNED(ctx, pl, (k_reduce_smem32<false, true>), (k_reduce_smem32<false, false>), d_xy,
+                                   n, g, w, pl.stages, d_L);
+            ctx->variant = pl.tma ? "smem32+tma" : "smem32";
+            return CHP_OK;
         }
-        k_filter_build<<<(ngroups + 255) / 256, 256, 0, ctx->stream>>>(d_L, w, gshift, 1, ys,
-                                                                      (uint32_t*)ctx->filter.p, ngroups);
-        CHP_LAUNCHED(ctx);
-        if (n > warm) {
-            const size_t smem = (size_t)ngroups * 4;
-            auto fn = validate ? k_reduce_filter<true> : k_reduce_filter<false>;
-            CHP_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            const int blocks = blocks_for(ctx, (const void*)fn, smem, 2);
-            fn<<<blocks, kThreads, smem, ctx->stream>>>(d_xy + 2 * warm, n - warm, g, w, gshift, 1, ys,
-                                                        (const uint32_t*)ctx->filter.p, ngroups, d_L);
+        case V_SMEM16: {
+            const Plan pl = plan_for(ctx, (size_t)w * 4, flags, false);
+            if (validate)
+                CHP_LAUNCH_PLANNED(ctx, pl, (k_reduce_smem16<true, true>), (k_reduce_smem16<true, false>), d_xy, n,
+                                   g, w, 1, pl.stages, d_L);
+            else
+                CHP_LAUNCH_PLANNED(ctx, pl, (k_reduce_smem16<false, true>), (k_reduce_smem16<false, false>), d_xy,
+                                   n, g, w, 1, pl.stages, d_L);
+            ctx->variant = pl.tma ? "smem16+tma" : "smem16";
+            return CHP_OK;
+        }
+        case V_FILTER8: {
+            // Warm-up prefix through L2, per-column snapshot, learning pass.
+            uint32_t ys = 0;
+            while ((uint64_t)(q - 1) >> ys > 255) ++ys;
+            const uint32_t wpad = (w + 7) & ~7u;
+            int rc = chp_ensure(ctx, ctx->filter, (size_t)wpad * 2 + 16);
+            if (rc) return rc;
+            const uint64_t warm = std::min<uint64_t>(n, n / 64) & ~1ull;
+            if ((rc = launch_global(d_xy, warm))) return rc;
+            k_filter8_build<<<(w + 255) / 256, 256, 0, ctx->stream>>>(d_L, w, ys, (uint16_t*)ctx->filter.p);
             CHP_LAUNCHED(ctx);
+            if (n > warm) {
+                const Plan pl = plan_for(ctx, (size_t)wpad * 2, flags, false);
+                CHP_LAUNCH_PLANNED(ctx, pl, k_reduce_filter8<true>, k_reduce_filter8<false>, d_xy + 2 * warm,
+                                   n - warm, g, w, ys, (const uint16_t*)ctx->filter.p, pl.stages, d_L);
+            }
+            ctx->variant = "filter8";
+            return CHP_OK;
         }
-        ctx->variant = "filter";
-        return CHP_OK;
+        case V_FILTER: {
+            const size_t fbudget = (flags & CHP_REDUCE_FILTER_SMALL) ? 100 * 1024 : budget;
+            int rc;
+            if (flags & CHP_REDUCE_FILTER16)
+                rc = validate ? run_group_filter<uint32_t, true>(ctx, d_xy, n, g, w, q, flags, fbudget, d_L)
+                              : run_group_filter<uint32_t, false>(ctx, d_xy, n, g, w, q, flags, fbudget, d_L);
+            else
+                rc = validate ? run_group_filter<uint16_t, true>(ctx, d_xy, n, g, w, q, flags, fbudget, d_L)
+                              : run_group_filter<uint16_t, false>(ctx, d_xy, n, g, w, q, flags, fbudget, d_L);
+            if (rc) return rc;
+            ctx->variant = (flags & CHP_REDUCE_FILTER16) ? "filter16" : "filter";
+            return CHP_OK;
+        }
+        default: {
+            int rc = launch_global(d_xy, n);
+            if (rc) return rc;
+            ctx->variant = "global";
+            return CHP_OK;
+        }
     }
-    auto fn = validate ? k_reduce_global<true> : k_reduce_global<false>;
-    const int blocks = blocks_for(ctx, (const void*)fn, 0, 4);
-    fn<<<blocks, kThreads, 0, ctx->stream>>>(d_xy, n, g, w, d_L);
-    CHP_LAUNCHED(ctx);
-    ctx->variant = "global";
-    return CHP_OK;
 }
 
 extern "C" int chp_check(chp_ctx* ctx, const int32_t* d_L, int64_t width) {

@@ -23,6 +23,8 @@ VARIANTS = {
     "global": _lib.REDUCE_FORCE_GLOBAL,
     "smem32": _lib.REDUCE_FORCE_SMEM32,
     "filter": _lib.REDUCE_FORCE_FILTER,
+    "filter8": _lib.REDUCE_FORCE_FILTER8,
+    "smem16": _lib.REDUCE_FORCE_SMEM16,
 }
 
 
