@@ -151,6 +151,10 @@ int chp_bounds(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int32_t* d_out4);
 int chp_translate(chp_ctx* ctx, const int32_t* d_in, uint64_t n, int32_t dx,
                   int32_t dy, int32_t* d_out);
 
+/* translate on HOST buffers (kernels::translate): H2D, kernel, D2H. */
+int chp_translate_host(chp_ctx* ctx, const int32_t* h_in, uint64_t n, int32_t dx,
+                       int32_t dy, int32_t* h_out);
+
 /* ------------------------------------------------ host-buffer pipelines
  * Inputs and outputs in HOST memory; pinned inputs are copied directly,
  * pageable ones through the context's pinned staging.  The copy of chunk

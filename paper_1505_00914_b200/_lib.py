@@ -58,6 +58,7 @@ def load() -> ctypes.CDLL:
         "chp_hull": (c_int, [vp, vp, vp, vp, c_int64, c_int, vp, vp]),
         "chp_bounds": (c_int, [vp, vp, c_uint64, vp]),
         "chp_translate": (c_int, [vp, vp, c_uint64, c_int32, c_int32, vp]),
+        "chp_translate_host": (c_int, [vp, vp, c_uint64, c_int32, c_int32, vp]),
         "chp_pipeline_host": (c_int, [vp, vp, c_uint64, c_int64, c_int64, vp, vp, vp, vp, vp, vp]),
         "chp_precondition_host": (c_int, [vp, vp, c_uint64, vp, vp, vp, vp, vp, vp]),
         "chp_generate": (c_int, [vp, c_int, c_uint64, c_int64, c_uint64, c_uint64, vp]),
@@ -75,6 +76,6 @@ def load() -> ctypes.CDLL:
 ABI_SYMBOLS = (
     "chp_ctx_create", "chp_ctx_destroy", "chp_last_error", "chp_ctx_set_stream", "chp_ctx_use_own_stream", "chp_ctx_stream",
     "chp_ctx_sync", "chp_launch_count", "chp_last_variant", "chp_dl_len", "chp_reduce", "chp_dl_init",
-    "chp_check", "chp_dl_from_pairs", "chp_polyline_host", "chp_compact", "chp_ns_chain", "chp_hull", "chp_bounds", "chp_translate",
+    "chp_check", "chp_dl_from_pairs", "chp_polyline_host", "chp_compact", "chp_ns_chain", "chp_hull", "chp_bounds", "chp_translate", "chp_translate_host",
     "chp_pipeline_host", "chp_precondition_host", "chp_generate", "chp_generate_host",
 )

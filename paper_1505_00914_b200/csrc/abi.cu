@@ -224,6 +224,25 @@ int chp_pipeline_host(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t wid
                        h_chain != nullptr || h_hull != nullptr);
 }
 
+int chp_translate_host(chp_ctx* ctx, const int32_t* h_in, uint64_t n, int32_t dx, int32_t dy, int32_t* h_out) {
+    if (!ctx) return CHP_EINVAL;
+    if (n == 0) return CHP_OK;
+    CHP_CUDA(ctx, cudaSetDevice(ctx->device));
+    DevBuf buf;
+    int rc = chp_ensure(ctx, buf, (size_t)n * 8);
+    if (rc) return rc;
+    cudaError_t e = cudaMemcpyAsync(buf.p, h_in, (size_t)n * 8, cudaMemcpyHostToDevice, ctx->stream);
+    if (e == cudaSuccess) {
+        rc = chp_translate(ctx, (const int32_t*)buf.p, n, dx, dy, (int32_t*)buf.p);
+        if (!rc) e = cudaMemcpyAsync(h_out, buf.p, (size_t)n * 8, cudaMemcpyDeviceToHost, ctx->stream);
+        if (!rc && e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    }
+    free_buf(buf);
+    if (rc) return rc;
+    if (e != cudaSuccess) return chp_cuda_fail(ctx, e, "translate_host");
+    return CHP_OK;
+}
+
 int chp_polyline_host(chp_ctx* ctx, const int32_t* h_Lpairs, int64_t width, int64_t major_off, int64_t minor_off,
                       int swapped, int32_t* h_chain, int64_t* h_s) {
     if (!ctx) return CHP_EINVAL;
