@@ -447,7 +447,9 @@ __global__ void __launch_bounds__(kThreads) k_reduce_filter(const int32_t* __res
         const uint32_t d = (uint32_t)y - (uint32_t)ybase;
         const uint32_t u = d >> ys;
         const uint32_t fa = w & HM, fb = w >> H;
-        const bool in = d <= ulim;
+        // Only a usable word (fa <= fb) bounds the group; the empty word
+        // (fa = all ones, fb = 0) says nothing about either side.
+        const bool in = d <= ulim && fa <= fb;
         const bool above_lo = in && u >= fa;  // y >= max_lo of the group
         const bool below_hi = in && u <= fb;  // y <= min_hi of the group
         if (above_lo && below_hi) return;
