@@ -19,6 +19,7 @@ REDUCE_FORCE_SMEM32 = 8
 REDUCE_FORCE_FILTER = 16
 REDUCE_FORCE_FILTER8 = 32
 REDUCE_FORCE_SMEM16 = 64
+REDUCE_FORCE_SAMPLED = 8192
 
 _lib = None
 

@@ -32,6 +32,7 @@ struct chp_ctx {
     DevBuf tile_status;  // K3 decoupled look-back status words
     DevBuf hull_a, hull_b, hull_cnt_a, hull_cnt_b;
     DevBuf filter;       // K1 filter snapshot
+    DevBuf sample;       // K1 sampled filter: per-CTA learned tables
     DevBuf dl;           // host pipeline: device-form L
     DevBuf counts;       // host pipeline: int64[8]
     DevBuf chain, lower, upper, hull, occ, lpairs;

@@ -85,6 +85,8 @@ __device__ __forceinline__ void for_each_group(const int32_t* __restrict__ xy, u
     // full-mask __syncwarp below is always matched.
     const uint64_t last = 31 - (threadIdx.x & 31);
     if (i + last + 3 * stride < sp.nvec) {
+        // (A ping-pong variant without the register copies below measured
+        // 2x slower for smem16 on B200 -- kept simple.)
         int4 a = ld_stream(v + i), b = ld_stream(v + i + stride);
         int4 c = ld_stream(v + i + 2 * stride), d = ld_stream(v + i + 3 * stride);
         for (;;) {
@@ -111,6 +113,64 @@ __device__ __forceinline__ void for_each_group(const int32_t* __restrict__ xy, u
     for (; i < sp.nvec; i += stride) {
         const int4 a = ld_stream(v + i);
         f(a.x, a.y); f(a.z, a.w);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (sp.head) f(xy[0], xy[1]);
+        if (sp.tail) f(xy[2 * (n - 1)], xy[2 * (n - 1) + 1]);
+    }
+}
+
+// Ping-pong form of the same loop: two register sets alternate, so no
+// per-group register copies.  Measured per kernel: +8% for the sampled
+// filter (C2), -50% for smem16 (C3/C5), so only k_reduce_sampled uses it.
+template <typename F>
+__device__ __forceinline__ void for_each_point_pp(const int32_t* __restrict__ xy, uint64_t n, F&& f) {
+    const Split sp = split_points(xy, n);
+    const int4* __restrict__ v = reinterpret_cast<const int4*>(xy + 2 * sp.head);
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t last = 31 - (threadIdx.x & 31);
+    auto g8 = [&](const int4& a, const int4& b, const int4& c, const int4& d) {
+        f(a.x, a.y); f(a.z, a.w);
+        f(b.x, b.y); f(b.z, b.w);
+        f(c.x, c.y); f(c.z, c.w);
+        f(d.x, d.y); f(d.z, d.w);
+    };
+    if (i + last + 3 * stride < sp.nvec) {
+        int4 a = ld_stream(v + i), b = ld_stream(v + i + stride);
+        int4 c = ld_stream(v + i + 2 * stride), d = ld_stream(v + i + 3 * stride);
+        int4 a2, b2, c2, d2;
+        for (;;) {
+            uint64_t nx = i + 4 * stride;
+            bool more = nx + last + 3 * stride < sp.nvec;
+            if (more) {
+                a2 = ld_stream(v + nx);
+                b2 = ld_stream(v + nx + stride);
+                c2 = ld_stream(v + nx + 2 * stride);
+                d2 = ld_stream(v + nx + 3 * stride);
+            }
+            g8(a, b, c, d);
+            __syncwarp();
+            i = nx;
+            if (!more) break;
+            nx = i + 4 * stride;
+            more = nx + last + 3 * stride < sp.nvec;
+            if (more) {
+                a = ld_stream(v + nx);
+                b = ld_stream(v + nx + stride);
+                c = ld_stream(v + nx + 2 * stride);
+                d = ld_stream(v + nx + 3 * stride);
+            }
+            g8(a2, b2, c2, d2);
+            __syncwarp();
+            i = nx;
+            if (!more) break;
+        }
+    }
+    for (; i < sp.nvec; i += stride) {
+        const int4 a = ld_stream(v + i);
+        f(a.x, a.y);
+        f(a.z, a.w);
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         if (sp.head) f(xy[0], xy[1]);
@@ -479,6 +539,110 @@ __global__ void __launch_bounds__(kThreads) k_reduce_filter(const int32_t* __res
     flag_error(bad, DL, width);
 }
 
+// ------------------------------------------------------------ sampled
+// Per-column filter built from a sample, exact by construction (mid-size p,
+// DESIGN.md "sampled filter").  Buckets u = (y-1) >> ys with ys chosen so
+// that u <= 254.
+//  1. k_sample_learn: each CTA folds its share of a sample (a prefix of the
+//     input) into a private table of (ua, ub) = (min, max) bucket per column
+//     with plain, racy shared-memory stores -- no atomics, no global traffic.
+//     Every stored endpoint is the bucket of an actual sample point (a lost
+//     race only narrows the interval).  Tables go to scratch.
+//  2. k_sample_merge: per column ua = min, ub = max over the CTA tables; the
+//     main-pass word is the STRICT interior: lo = ua + 1, span = ub - lo
+//     (>= 0), skip iff (u - lo) < span (unsigned) i.e. ua < u < ub.
+//  3. k_reduce_sampled: one pass over ALL points.  A skipped point lies
+//     strictly between two sample points of its column, which are never
+//     skipped themselves (they sit in the boundary buckets) and so reach L:
+//     the skipped point cannot be an extreme.  A miss with span > 0 lies at
+//     or beyond one boundary bucket, so only that side can move: one RED,
+//     then the word widens to the point's bucket.
+__global__ void __launch_bounds__(kThreads) k_sample_learn(const int32_t* __restrict__ xy, uint64_t n, Geo g,
+                                                           uint32_t width, uint32_t wpad, uint32_t ys,
+                                                           uint16_t* __restrict__ scratch) {
+    extern __shared__ uint4 smem4[];
+    uint16_t* T = reinterpret_cast<uint16_t*>(smem4);
+    for (uint32_t c = threadIdx.x; c < wpad; c += blockDim.x) T[c] = 0x00FF;  // ua = 255 > ub = 0: empty
+    __syncthreads();
+    auto f = [&](int32_t x, int32_t y) {
+        uint32_t s;
+        if (!accept<true>(g, x, y, s)) return;  // the main pass flags it
+        const uint32_t u = ((uint32_t)y - 1u) >> ys;
+        const uint32_t w = T[s];
+        const uint32_t ua = min(w & 0xFFu, u), ub = max(w >> 8, u);
+        const uint32_t nw = ua | (ub << 8);
+        if (nw != w) T[s] = (uint16_t)nw;
+    };
+    for_each_point(xy, n, f);
+    __syncthreads();
+    uint4* dst = reinterpret_cast<uint4*>(scratch + (size_t)blockIdx.x * wpad);
+    for (uint32_t i = threadIdx.x; i < wpad / 8; i += blockDim.x) dst[i] = smem4[i];
+}
+
+__global__ void k_sample_merge(const uint16_t* __restrict__ scratch, uint32_t ntables, uint32_t width,
+                               uint32_t wpad, uint16_t* __restrict__ F) {
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= wpad) return;
+    uint32_t ua = 255, ub = 0;
+    for (uint32_t t = 0; t < ntables; ++t) {
+        const uint32_t w = scratch[(size_t)t * wpad + c];
+        ua = min(ua, w & 0xFFu);
+        ub = max(ub, w >> 8);
+    }
+    uint16_t word = 0x00FF;  // lo = 255, span = 0: never skip
+    if (c < width && ua <= ub) {
+        const uint32_t lo = ua + 1;  // <= 255 because buckets stop at 254
+        const uint32_t span = ub > lo ? ub - lo : 0;
+        word = (uint16_t)(lo | (span << 8));
+    }
+    F[c] = word;
+}
+
+template <bool TMA>
+__global__ void __launch_bounds__(kThreads) k_reduce_sampled(const int32_t* __restrict__ xy, uint64_t n, Geo g,
+                                                             uint32_t width, uint32_t wpad, uint32_t ys,
+                                                             const uint16_t* __restrict__ F, int stages,
+                                                             int* __restrict__ DL) {
+    extern __shared__ uint4 smem4[];
+    uint16_t* T = reinterpret_cast<uint16_t*>(smem4);
+    uint8_t* ring = reinterpret_cast<uint8_t*>(smem4) + table_span((size_t)wpad * 2);
+    {
+        const uint4* F4 = reinterpret_cast<const uint4*>(F);
+        for (uint32_t i = threadIdx.x; i < wpad / 8; i += blockDim.x) smem4[i] = __ldcg(F4 + i);
+    }
+    __syncthreads();
+    bool bad = false;
+    auto f = [&](int32_t x, int32_t y) {
+        const uint32_t s = slot_of(x, g.base);
+        const uint32_t ym1 = (uint32_t)y - 1u;
+        if (s >= g.wcheck || ym1 >= g.qmax) {
+            bad = true;
+            return;
+        }
+        const uint32_t w = T[s];
+        const uint32_t lo = w & 0xFFu, span = w >> 8;
+        const uint32_t u = ym1 >> ys;
+        if (u - lo < span) return;  // strictly inside the sample's buckets
+        if (span == 0) {            // nothing known: both sides may move
+            red_min(DL + 2ull * s, y);
+            red_min(DL + 2ull * s + 1, ~y);
+            return;
+        }
+        if (u < lo) {  // at/below the lower boundary bucket: only lo moves
+            red_min(DL + 2ull * s, y);
+            if (u + 1 < lo) T[s] = (uint16_t)((u + 1) | ((lo + span - u - 1) << 8));
+        } else {  // at/above the upper boundary bucket: only hi moves
+            red_min(DL + 2ull * s + 1, ~y);
+            if (u > lo + span) T[s] = (uint16_t)(lo | ((u - lo) << 8));
+        }
+    };
+    if (TMA)
+        stream_points<true>(xy, n, ring, stages, per_point4(f), f);
+    else
+        for_each_point_pp(xy, n, f);
+    flag_error(bad, DL, width);
+}
+
 // ------------------------------------------------------------ filter8
 // Per-column learning filter for mid-size p (one 16-bit word per column:
 // bits 0-7 qa = ceil((lo-1) / 2^ys), bits 8-15 qb = floor(hi / 2^ys) - 1,
@@ -692,14 +856,19 @@ extern "C" int chp_reduce(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t
     const bool yknown = validate && q >= 1;  // every accepted y is in [1, q]
     const bool fits_f8 = yknown && (size_t)((w + 7) & ~7u) * 2 <= budget;
 
-    enum { V_GLOBAL, V_SMEM32, V_SMEM16, V_FILTER8, V_FILTER } v;
+    const uint32_t wpad8 = (w + 7) & ~7u;
+    const bool fits_sampled = yknown && (size_t)wpad8 * 2 <= budget;
+
+    enum { V_GLOBAL, V_SMEM32, V_SMEM16, V_FILTER8, V_FILTER, V_SAMPLED } v;
     if (flags & CHP_REDUCE_FORCE_GLOBAL) v = V_GLOBAL;
+    else if ((flags & CHP_REDUCE_FORCE_SAMPLED) && fits_sampled) v = V_SAMPLED;
     else if ((flags & CHP_REDUCE_FORCE_SMEM32) && fits32) v = V_SMEM32;
     else if ((flags & CHP_REDUCE_FORCE_SMEM16) && fits16) v = V_SMEM16;
     else if ((flags & CHP_REDUCE_FORCE_FILTER8) && fits_f8) v = V_FILTER8;
     else if ((flags & CHP_REDUCE_FORCE_FILTER) && yknown) v = V_FILTER;
     else if (fits16) v = V_SMEM16;  // measured: 1.05-1.24x smem32 (C3, C5)
     else if (fits32) v = V_SMEM32;
+    else if (fits_sampled) v = V_SAMPLED;
     else if (yknown) v = V_FILTER;
     else v = V_GLOBAL;
 
@@ -755,6 +924,31 @@ extern "C" int chp_reduce(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t
                                    n - warm, g, w, ys, (const uint16_t*)ctx->filter.p, pl.stages, d_L);
             }
             ctx->variant = "filter8";
+            return CHP_OK;
+        }
+        case V_SAMPLED: {
+            // Sample pass (prefix n/16) -> merged strict-interior table -> one
+            // pass over all n points.
+            uint32_t ys = 0;
+            while ((uint64_t)(q - 1) >> ys > 254) ++ys;
+            const size_t tbytes = (size_t)wpad8 * 2;
+            const int sblocks = ctx->sm_count;
+            int rc = chp_ensure(ctx, ctx->sample, (size_t)sblocks * tbytes + 16);
+            if (!rc) rc = chp_ensure(ctx, ctx->filter, tbytes + 16);
+            if (rc) return rc;
+            const uint64_t ns = std::min<uint64_t>(n, std::max<uint64_t>(n / 16, 2)) & ~1ull;
+            CHP_CUDA(ctx, cudaFuncSetAttribute(k_sample_learn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)table_span(tbytes)));
+            k_sample_learn<<<sblocks, kThreads, table_span(tbytes), ctx->stream>>>(d_xy, ns, g, w, wpad8, ys,
+                                                                                 (uint16_t*)ctx->sample.p);
+            CHP_LAUNCHED(ctx);
+            k_sample_merge<<<(wpad8 + 255) / 256, 256, 0, ctx->stream>>>((const uint16_t*)ctx->sample.p, sblocks, w,
+                                                                         wpad8, (uint16_t*)ctx->filter.p);
+            CHP_LAUNCHED(ctx);
+            const Plan pl = plan_for(ctx, tbytes, flags, false);
+            CHP_LAUNCH_PLANNED(ctx, pl, k_reduce_sampled<true>, k_reduce_sampled<false>, d_xy, n, g, w, wpad8, ys,
+                               (const uint16_t*)ctx->filter.p, pl.stages, d_L);
+            ctx->variant = "sampled";
             return CHP_OK;
         }
         case V_FILTER: {

@@ -25,6 +25,8 @@ VARIANTS = {
     "filter": _lib.REDUCE_FORCE_FILTER,
     "filter8": _lib.REDUCE_FORCE_FILTER8,
     "smem16": _lib.REDUCE_FORCE_SMEM16,
+    "sampled": _lib.REDUCE_FORCE_SAMPLED,
+    "smem16_tma": _lib.REDUCE_FORCE_SMEM16 | 4096,
 }
 
 
@@ -199,7 +201,7 @@ def test_full_size_properties(ctx, config):
         pytest.skip("not enough device memory")
     d = ctx.generate(config, seed, p, n)
     ref_dl = ctx.reduce(d, p, q=p).clone()
-    for flags in (_lib.REDUCE_FORCE_GLOBAL, _lib.REDUCE_FORCE_FILTER):
+    for flags in (_lib.REDUCE_FORCE_GLOBAL, _lib.REDUCE_FORCE_FILTER, _lib.REDUCE_FORCE_SAMPLED):
         assert torch.equal(ctx.reduce(d, p, q=p, flags=flags), ref_dl)
     half = n // 2
     a = ctx.reduce(d[:half], p, q=p).clone()
