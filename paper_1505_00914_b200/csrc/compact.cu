@@ -20,8 +20,11 @@
 
 namespace {
 
-constexpr int kCT = 256;      // threads per tile
-constexpr int kItems = 8;      // slots per thread
+// 128 threads x 4 slots: 512-slot tiles, so p = 65536 spreads over 128 CTAs
+// (2048-slot tiles left 32 CTAs latency-bound: 10.5 us at C2).
+constexpr int kCT = 128;       // threads per tile
+constexpr int kItems = 4;      // slots per thread
+constexpr int kLanesPerWord = 64 / kItems;
 constexpr int kTile = kCT * kItems;
 
 constexpr unsigned long long kFlagAgg = 1ull << 62;
@@ -165,13 +168,13 @@ __global__ void __launch_bounds__(kCT) k_compact(const int* __restrict__ DL, uin
         V += 1;
     }
     if (occ) {
-        // 8 lanes x 8 slots = one 64-bit word (slot0 of lane 8k is 64-aligned).
-        unsigned long long word = (unsigned long long)vmask << (8 * (lane & 7));
-        word |= __shfl_xor_sync(0xffffffffu, word, 1);
-        word |= __shfl_xor_sync(0xffffffffu, word, 2);
-        word |= __shfl_xor_sync(0xffffffffu, word, 4);
+        // kLanesPerWord lanes x kItems slots = one 64-bit word (the first
+        // slot of lane kLanesPerWord*k is 64-aligned).
+        unsigned long long word = (unsigned long long)vmask << (kItems * (lane % kLanesPerWord));
+#pragma unroll
+        for (int o = 1; o < kLanesPerWord; o <<= 1) word |= __shfl_xor_sync(0xffffffffu, word, o);
         const uint64_t wi = slot0 >> 6;
-        if ((lane & 7) == 0 && wi * 64 < width) occ[wi] = word;
+        if (lane % kLanesPerWord == 0 && wi * 64 < width) occ[wi] = word;
     }
     if (tile == ntiles - 1 && threadIdx.x == kCT - 1) {
         // The last tile's last thread holds the totals.

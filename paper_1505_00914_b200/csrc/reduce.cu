@@ -551,12 +551,25 @@ __global__ void __launch_bounds__(kThreads) k_reduce_filter(const int32_t* __res
 //     the skipped point cannot be an extreme.  A miss with span > 0 lies at
 //     or beyond one boundary bucket, so only that side can move: one RED,
 //     then the word widens to the point's bucket.
+// Tables are dumped as (ua, 255 - ub) so the merge is one byte-wise min.
+// With init_dl the kernel also initialises DL (the main pass runs after it in
+// stream order), saving the separate k_dl_init launch.
 __global__ void __launch_bounds__(kThreads) k_sample_learn(const int32_t* __restrict__ xy, uint64_t n, Geo g,
                                                            uint32_t width, uint32_t wpad, uint32_t ys,
-                                                           uint16_t* __restrict__ scratch) {
+                                                           uint16_t* __restrict__ scratch, int* __restrict__ DL,
+                                                           int init_dl) {
     extern __shared__ uint4 smem4[];
     uint16_t* T = reinterpret_cast<uint16_t*>(smem4);
     for (uint32_t c = threadIdx.x; c < wpad; c += blockDim.x) T[c] = 0x00FF;  // ua = 255 > ub = 0: empty
+    if (init_dl) {
+        const uint64_t words = 2ull * width;
+        for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < words; i += (uint64_t)gridDim.x * blockDim.x)
+            DL[i] = CHP_EMPTY;
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            DL[words] = 0;
+            DL[words + 1] = 0;
+        }
+    }
     __syncthreads();
     auto f = [&](int32_t x, int32_t y) {
         uint32_t s;
@@ -570,26 +583,69 @@ __global__ void __launch_bounds__(kThreads) k_sample_learn(const int32_t* __rest
     for_each_point(xy, n, f);
     __syncthreads();
     uint4* dst = reinterpret_cast<uint4*>(scratch + (size_t)blockIdx.x * wpad);
-    for (uint32_t i = threadIdx.x; i < wpad / 8; i += blockDim.x) dst[i] = smem4[i];
+    for (uint32_t i = threadIdx.x; i < wpad / 8; i += blockDim.x) {
+        uint4 q = smem4[i];
+        q.x ^= 0xFF00FF00u;  // ub -> 255 - ub in the high byte of each word
+        q.y ^= 0xFF00FF00u;
+        q.z ^= 0xFF00FF00u;
+        q.w ^= 0xFF00FF00u;
+        dst[i] = q;
+    }
 }
 
-__global__ void k_sample_merge(const uint16_t* __restrict__ scratch, uint32_t ntables, uint32_t width,
-                               uint32_t wpad, uint16_t* __restrict__ F) {
-    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= wpad) return;
-    uint32_t ua = 255, ub = 0;
-    for (uint32_t t = 0; t < ntables; ++t) {
-        const uint32_t w = scratch[(size_t)t * wpad + c];
-        ua = min(ua, w & 0xFFu);
-        ub = max(ub, w >> 8);
+// Byte-wise min over the CTA tables: thread (x, y) folds tables y, y+8, ...
+// for 8 columns (one uint4), then the 8 partials meet in shared memory.
+constexpr int kMergeCols = 32;  // uint4 chunks per block (x)
+constexpr int kMergeSlices = 8; // table slices per block (y)
+
+__global__ void __launch_bounds__(kMergeCols * kMergeSlices) k_sample_merge(const uint16_t* __restrict__ scratch,
+                                                                           uint32_t ntables, uint32_t width,
+                                                                           uint32_t wpad, uint16_t* __restrict__ F) {
+    __shared__ uint4 part[kMergeSlices][kMergeCols];
+    const uint32_t chunk = blockIdx.x * kMergeCols + threadIdx.x;
+    const uint32_t nchunks = wpad / 8;
+    uint4 m = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+    if (chunk < nchunks) {
+        const uint4* src = reinterpret_cast<const uint4*>(scratch) + chunk;
+#pragma unroll 4
+        for (uint32_t t = threadIdx.y; t < ntables; t += kMergeSlices) {
+            const uint4 q = __ldcs(src + (size_t)t * nchunks);
+            m.x = __vminu4(m.x, q.x);
+            m.y = __vminu4(m.y, q.y);
+            m.z = __vminu4(m.z, q.z);
+            m.w = __vminu4(m.w, q.w);
+        }
     }
-    uint16_t word = 0x00FF;  // lo = 255, span = 0: never skip
-    if (c < width && ua <= ub) {
-        const uint32_t lo = ua + 1;  // <= 255 because buckets stop at 254
-        const uint32_t span = ub > lo ? ub - lo : 0;
-        word = (uint16_t)(lo | (span << 8));
+    part[threadIdx.y][threadIdx.x] = m;
+    __syncthreads();
+    if (threadIdx.y != 0 || chunk >= nchunks) return;
+    for (int k = 1; k < kMergeSlices; ++k) {
+        const uint4 q = part[k][threadIdx.x];
+        m.x = __vminu4(m.x, q.x);
+        m.y = __vminu4(m.y, q.y);
+        m.z = __vminu4(m.z, q.z);
+        m.w = __vminu4(m.w, q.w);
     }
-    F[c] = word;
+    const uint32_t words[4] = {m.x, m.y, m.z, m.w};
+    uint32_t out[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        uint32_t o = 0;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint32_t c = chunk * 8 + k * 2 + h;
+            const uint32_t w16 = (words[k] >> (16 * h)) & 0xFFFFu;
+            const uint32_t ua = w16 & 0xFFu, ub = 255u - (w16 >> 8);
+            uint32_t word = 0x00FF;  // lo = 255, span = 0: never skip
+            if (c < width && ua <= ub) {
+                const uint32_t lo = ua + 1;  // <= 255 because buckets stop at 254
+                word = lo | ((ub > lo ? ub - lo : 0) << 8);
+            }
+            o |= word << (16 * h);
+        }
+        out[k] = o;
+    }
+    reinterpret_cast<uint4*>(F)[chunk] = make_uint4(out[0], out[1], out[2], out[3]);
 }
 
 __device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
@@ -873,11 +929,8 @@ extern "C" int chp_reduce(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t
     if (x_off + 1 < (int64_t)INT32_MIN || x_off > (int64_t)INT32_MAX)
         return chp_einval(ctx, "reduce: x offset outside the int32 range");
     const bool validate = !(flags & CHP_REDUCE_NO_VALIDATE);
-    if (!(flags & CHP_REDUCE_ACCUMULATE)) {
-        int rc = chp_dl_init(ctx, d_L, width);
-        if (rc) return rc;
-    }
-    if (n == 0) return CHP_OK;
+    const bool need_init = !(flags & CHP_REDUCE_ACCUMULATE);
+    if (n == 0) return need_init ? chp_dl_init(ctx, d_L, width) : CHP_OK;
 
     Geo g;
     g.base = (uint32_t)(int32_t)(x_off + 1);
@@ -907,6 +960,12 @@ extern "C" int chp_reduce(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t
     else if (fits_sampled) v = V_SAMPLED;
     else if (yknown) v = V_FILTER;
     else v = V_GLOBAL;
+
+    // The sampled variant initialises DL inside its sample pass.
+    if (need_init && v != V_SAMPLED) {
+        int rc = chp_dl_init(ctx, d_L, width);
+        if (rc) return rc;
+    }
 
     auto launch_global = [&](const int32_t* p, uint64_t m) -> int {
         if (m == 0) return CHP_OK;
@@ -975,11 +1034,13 @@ extern "C" int chp_reduce(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t
             const uint64_t ns = std::min<uint64_t>(n, std::max<uint64_t>(n / 16, 2)) & ~1ull;
             CHP_CUDA(ctx, cudaFuncSetAttribute(k_sample_learn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                (int)table_span(tbytes)));
-            k_sample_learn<<<sblocks, kThreads, table_span(tbytes), ctx->stream>>>(d_xy, ns, g, w, wpad8, ys,
-                                                                                 (uint16_t*)ctx->sample.p);
+            k_sample_learn<<<sblocks, kThreads, table_span(tbytes), ctx->stream>>>(
+                d_xy, ns, g, w, wpad8, ys, (uint16_t*)ctx->sample.p, d_L, need_init ? 1 : 0);
             CHP_LAUNCHED(ctx);
-            k_sample_merge<<<(wpad8 + 255) / 256, 256, 0, ctx->stream>>>((const uint16_t*)ctx->sample.p, sblocks, w,
-                                                                         wpad8, (uint16_t*)ctx->filter.p);
+            const uint32_t nchunks = wpad8 / 8;
+            k_sample_merge<<<(nchunks + kMergeCols - 1) / kMergeCols, dim3(kMergeCols, kMergeSlices), 0,
+                             ctx->stream>>>((const uint16_t*)ctx->sample.p, sblocks, w, wpad8,
+                                            (uint16_t*)ctx->filter.p);
             CHP_LAUNCHED(ctx);
             const Plan pl = plan_for(ctx, tbytes, flags, false);
             CHP_LAUNCH_PLANNED(ctx, pl, k_reduce_sampled<true>, k_reduce_sampled<false>, d_xy, n, g, w, wpad8, ys,
