@@ -123,21 +123,43 @@ __global__ void __launch_bounds__(kCT) k_compact(const int* __restrict__ DL, uin
             if (lane == 0) st_release(status + tile, pack_status(kFlagIncl, tile_agg));
         } else {
             if (lane == 0) st_release(status + tile, pack_status(kFlagAgg, tile_agg));
-            long long pred = (long long)tile - 1;
+            // Look back over a window of 256 predecessors at once (8 per
+            // lane, all loads in flight together): every tile publishes its
+            // aggregate right after its local scan, so one window usually
+            // settles the prefix in a single L2 round trip instead of a
+            // chain of 32-tile steps.  Indices below 0 read as an
+            // inclusive zero.
+            constexpr int kPer = 8;
+            long long top = (long long)tile - 1;
             for (;;) {
-                const long long t = pred - lane;
-                unsigned long long st = t >= 0 ? ld_acquire(status + t) : kFlagIncl;
-                while (__any_sync(0xffffffffu, (st >> 62) == 0)) {
-                    if ((st >> 62) == 0) st = ld_acquire(status + t);
+                unsigned long long st[kPer];
+                long long idx[kPer];
+#pragma unroll
+                for (int k = 0; k < kPer; ++k) {
+                    idx[k] = top - lane - 32 * k;
+                    st[k] = idx[k] >= 0 ? ld_acquire(status + idx[k]) : kFlagIncl;
                 }
-                const unsigned incl_lanes = __ballot_sync(0xffffffffu, (st >> 62) == 2);
-                const int stop = incl_lanes ? __ffs(incl_lanes) - 1 : 31;
-                unsigned long long val = (lane <= stop) ? unpack_cv(st) : 0ull;
+#pragma unroll
+                for (int k = 0; k < kPer; ++k)
+                    while ((st[k] >> 62) == 0) st[k] = ld_acquire(status + idx[k]);
+                long long best = LLONG_MIN;  // nearest inclusive predecessor in the window
+#pragma unroll
+                for (int k = 0; k < kPer; ++k)
+                    if ((st[k] >> 62) == 2 && idx[k] > best) best = idx[k];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const long long b = __shfl_xor_sync(0xffffffffu, best, o);
+                    best = b > best ? b : best;
+                }
+                unsigned long long val = 0;
+#pragma unroll
+                for (int k = 0; k < kPer; ++k)
+                    if (idx[k] >= best && idx[k] >= 0) val += unpack_cv(st[k]);
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
                 excl += val;
-                if (incl_lanes) break;
-                pred -= 32;
+                if (best != LLONG_MIN) break;
+                top -= 32 * kPer;
             }
             if (lane == 0) st_release(status + tile, pack_status(kFlagIncl, excl + tile_agg));
         }

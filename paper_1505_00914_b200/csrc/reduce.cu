@@ -595,8 +595,8 @@ __global__ void __launch_bounds__(kThreads) k_sample_learn(const int32_t* __rest
 
 // Byte-wise min over the CTA tables: thread (x, y) folds tables y, y+8, ...
 // for 8 columns (one uint4), then the 8 partials meet in shared memory.
-constexpr int kMergeCols = 32;  // uint4 chunks per block (x)
-constexpr int kMergeSlices = 8; // table slices per block (y)
+constexpr int kMergeCols = 16;   // uint4 chunks per block (x)
+constexpr int kMergeSlices = 16; // table slices per block (y): ~10 loads in flight per thread
 
 __global__ void __launch_bounds__(kMergeCols * kMergeSlices) k_sample_merge(const uint16_t* __restrict__ scratch,
                                                                            uint32_t ntables, uint32_t width,
@@ -607,7 +607,7 @@ __global__ void __launch_bounds__(kMergeCols * kMergeSlices) k_sample_merge(cons
     uint4 m = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
     if (chunk < nchunks) {
         const uint4* src = reinterpret_cast<const uint4*>(scratch) + chunk;
-#pragma unroll 4
+#pragma unroll 5
         for (uint32_t t = threadIdx.y; t < ntables; t += kMergeSlices) {
             const uint4 q = __ldcs(src + (size_t)t * nchunks);
             m.x = __vminu4(m.x, q.x);
