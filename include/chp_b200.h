@@ -85,6 +85,7 @@ uint64_t chp_dl_len(int64_t width);
 #define CHP_REDUCE_NO_TMA 2048u     /* tuning: stream via registers, not the TMA ring */
 #define CHP_REDUCE_TMA 4096u        /* tuning: stream via the TMA bulk-copy ring */
 #define CHP_REDUCE_FORCE_SAMPLED 8192u /* testing: force the sampled per-column filter */
+#define CHP_REDUCE_FUSED 16384u     /* tuning: sampled filter as 1 cooperative kernel (grid barriers) */
 
 /* Algorithm 1 over n int32 (x,y) pairs at d_xy (8-byte aligned).  Slot of a
  * point is x - x_off - 1; a point is valid when that slot is in [0,width)

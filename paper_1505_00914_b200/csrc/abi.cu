@@ -154,6 +154,7 @@ int chp_ctx_create(int device, chp_ctx** out) {
     if (e == cudaSuccess)
         e = cudaDeviceGetAttribute(&ctx->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->l2_bytes, cudaDevAttrL2CacheSize, device);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->coop, cudaDevAttrCooperativeLaunch, device);
     if (e != cudaSuccess) {
         cudaGetLastError();
         delete ctx;
@@ -170,7 +171,7 @@ void chp_ctx_destroy(chp_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     cudaStreamSynchronize(ctx->copy_stream);
     DevBuf* bufs[] = {&ctx->tile_status, &ctx->hull_a, &ctx->hull_b, &ctx->hull_cnt_a, &ctx->hull_cnt_b,
-                      &ctx->filter, &ctx->sample, &ctx->dl, &ctx->counts, &ctx->chain, &ctx->lower, &ctx->upper,
+                      &ctx->filter, &ctx->sample, &ctx->gridbar, &ctx->dl, &ctx->counts, &ctx->chain, &ctx->lower, &ctx->upper,
                       &ctx->hull, &ctx->occ, &ctx->lpairs, &ctx->stage_dev[0], &ctx->stage_dev[1]};
     for (DevBuf* b : bufs) free_buf(*b);
     for (int b = 0; b < 2; ++b) {

@@ -33,6 +33,8 @@ struct chp_ctx {
     DevBuf hull_a, hull_b, hull_cnt_a, hull_cnt_b;
     DevBuf filter;       // K1 filter snapshot
     DevBuf sample;       // K1 sampled filter: per-CTA learned tables
+    DevBuf gridbar;      // grid barrier of the cooperative sampled kernel
+    int coop = 0;        // cudaDevAttrCooperativeLaunch
     DevBuf dl;           // host pipeline: device-form L
     DevBuf counts;       // host pipeline: int64[8]
     DevBuf chain, lower, upper, hull, occ, lpairs;

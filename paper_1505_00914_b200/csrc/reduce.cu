@@ -735,6 +735,187 @@ __global__ void __launch_bounds__(kThreads) k_reduce_sampled(const int32_t* __re
     flag_error(bad != 0, DL, width);
 }
 
+// ------------------------------------------------------- sampled, fused
+// The sampled pipeline as ONE cooperative kernel (all CTAs co-resident, one
+// per SM): sample pass -> grid barrier -> merge, each CTA owning 1/grid of
+// the columns -> grid barrier -> every CTA loads the merged table -> main
+// pass.  Saves two launch boundaries (ramp-down/ramp-up) and spreads the
+// merge over every SM.
+struct GridBar {
+    unsigned count;
+    unsigned gen;
+};
+
+__device__ __noinline__ void sampled_main_pass(const int32_t* __restrict__ xy, uint64_t n, Geo g, uint32_t width,
+                                               uint32_t ys, uint32_t tbase, int* __restrict__ DL);
+
+constexpr size_t kFusedMergeSmem = 16 * 64 * sizeof(uint4);  // phase B partials
+
+__device__ __forceinline__ void grid_barrier(GridBar* b) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned* vgen = &b->gen;
+        const unsigned g0 = *vgen;
+        __threadfence();
+        if (atomicAdd(&b->count, 1u) == gridDim.x - 1) {
+            atomicExch(&b->count, 0u);
+            __threadfence();
+            atomicAdd(&b->gen, 1u);
+        } else {
+            while (*vgen == g0) __nanosleep(64);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kThreads) k_sampled_fused(const int32_t* __restrict__ xy, uint64_t n, uint64_t ns,
+                                                            Geo g, uint32_t width, uint32_t wpad, uint32_t ys,
+                                                            uint16_t* __restrict__ scratch, uint16_t* __restrict__ F,
+                                                            int* __restrict__ DL, int init_dl, GridBar* bar) {
+    extern __shared__ uint4 smem4[];
+    uint16_t* T = reinterpret_cast<uint16_t*>(smem4);
+    const uint32_t nchunks = wpad / 8;
+    // ---- A: sample pass (as k_sample_learn) + DL init
+    for (uint32_t c = threadIdx.x; c < wpad; c += blockDim.x) T[c] = 0x00FF;
+    if (init_dl) {
+        const uint64_t words = 2ull * width;
+        for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < words;
+             i += (uint64_t)gridDim.x * blockDim.x)
+            DL[i] = CHP_EMPTY;
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            DL[words] = 0;
+            DL[words + 1] = 0;
+        }
+    }
+    __syncthreads();
+    for_each_point(xy, ns, [&](int32_t x, int32_t y) {
+        uint32_t s;
+        if (!accept<true>(g, x, y, s)) return;
+        const uint32_t u = ((uint32_t)y - 1u) >> ys;
+        const uint32_t w = T[s];
+        const uint32_t nw = min(w & 0xFFu, u) | (max(w >> 8, u) << 8);
+        if (nw != w) T[s] = (uint16_t)nw;
+    });
+    __syncthreads();
+    {
+        uint4* dst = reinterpret_cast<uint4*>(scratch) + (size_t)blockIdx.x * nchunks;
+        for (uint32_t i = threadIdx.x; i < nchunks; i += blockDim.x) {
+            uint4 q = smem4[i];
+            q.x ^= 0xFF00FF00u;
+            q.y ^= 0xFF00FF00u;
+            q.z ^= 0xFF00FF00u;
+            q.w ^= 0xFF00FF00u;
+            dst[i] = q;
+        }
+    }
+    grid_barrier(bar);
+    // ---- B: merge; this CTA owns chunks [c0, c1), 64 chunks x 16 slices
+    {
+        const uint32_t per = (nchunks + gridDim.x - 1) / gridDim.x;
+        const uint32_t c0 = blockIdx.x * per, c1 = min(nchunks, c0 + per);
+        uint4* part = smem4;  // [16][64] uint4, the table is reloaded in C
+        for (uint32_t base = c0; base < c1; base += 64) {
+            const uint32_t cl = threadIdx.x & 63, slice = threadIdx.x >> 6;
+            const uint32_t chunk = base + cl;
+            uint4 m = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+            if (chunk < c1) {
+                const uint4* src = reinterpret_cast<const uint4*>(scratch) + chunk;
+#pragma unroll 5
+                for (uint32_t t = slice; t < gridDim.x; t += 16) {
+                    const uint4 q = __ldcg(src + (size_t)t * nchunks);
+                    m.x = __vminu4(m.x, q.x);
+                    m.y = __vminu4(m.y, q.y);
+                    m.z = __vminu4(m.z, q.z);
+                    m.w = __vminu4(m.w, q.w);
+                }
+            }
+            part[slice * 64 + cl] = m;
+            __syncthreads();
+            if (slice == 0 && chunk < c1) {
+                for (int k = 1; k < 16; ++k) {
+                    const uint4 q = part[k * 64 + cl];
+                    m.x = __vminu4(m.x, q.x);
+                    m.y = __vminu4(m.y, q.y);
+                    m.z = __vminu4(m.z, q.z);
+                    m.w = __vminu4(m.w, q.w);
+                }
+                const uint32_t words[4] = {m.x, m.y, m.z, m.w};
+                uint32_t out[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    uint32_t o = 0;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const uint32_t c = chunk * 8 + k * 2 + h;
+                        const uint32_t w16 = (words[k] >> (16 * h)) & 0xFFFFu;
+                        const uint32_t ua = w16 & 0xFFu, ub = 255u - (w16 >> 8);
+                        uint32_t word = 0x00FF;
+                        if (c < width && ua <= ub) {
+                            const uint32_t lo = ua + 1;
+                            word = lo | ((ub > lo ? ub - lo : 0) << 8);
+                        }
+                        o |= word << (16 * h);
+                    }
+                    out[k] = o;
+                }
+                reinterpret_cast<uint4*>(F)[chunk] = make_uint4(out[0], out[1], out[2], out[3]);
+            }
+            __syncthreads();
+        }
+    }
+    grid_barrier(bar);
+    // ---- C: every CTA loads the merged table
+    {
+        const uint4* F4 = reinterpret_cast<const uint4*>(F);
+        for (uint32_t i = threadIdx.x; i < nchunks; i += blockDim.x) smem4[i] = __ldcg(F4 + i);
+    }
+    __syncthreads();
+    // ---- D: main pass (as k_reduce_sampled)
+    sampled_main_pass(xy, n, g, width, ys, (uint32_t)__cvta_generic_to_shared(smem4), DL);
+}
+
+// Phase D of k_sampled_fused, out of line (called once per CTA) so the hot
+// loop gets a register allocation of its own.
+__device__ __noinline__ void sampled_main_pass(const int32_t* __restrict__ xy, uint64_t n, Geo g, uint32_t width,
+                                               uint32_t ys, uint32_t tbase, int* __restrict__ DL) {
+    uint32_t bad = 0;
+    auto one = [&](int32_t x, int32_t y) {
+        const uint32_t s0 = slot_of(x, g.base);
+        const uint32_t ym1 = (uint32_t)y - 1u;
+        const bool ok = (s0 < g.wcheck) & (ym1 < g.qmax);
+        bad |= !ok;
+        const uint32_t s = ok ? s0 : 0u;
+        const uint32_t a = tbase + 2 * s;
+        const uint32_t w = lds_u16(a);
+        const uint32_t lo = w & 0xFFu, span = w >> 8;
+        const uint32_t u = ym1 >> ys;
+        if (!ok || u - lo < span) return;
+        if (span == 0) {
+            red_min(DL + 2ull * s, y);
+            red_min(DL + 2ull * s + 1, ~y);
+            return;
+        }
+        if (u < lo) {
+            red_min(DL + 2ull * s, y);
+            if (u + 1 < lo) sts_u16(a, (u + 1) | ((lo + span - u - 1) << 8));
+        } else {
+            red_min(DL + 2ull * s + 1, ~y);
+            if (u > lo + span) sts_u16(a, lo | ((u - lo) << 8));
+        }
+    };
+    for_each_group_pp(
+        xy, n,
+        [&](const int4& a, const int4& b, const int4& c, const int4& d) {
+            one(a.x, a.y); one(a.z, a.w);
+            one(b.x, b.y); one(b.z, b.w);
+            one(c.x, c.y); one(c.z, c.w);
+            one(d.x, d.y); one(d.z, d.w);
+        },
+        one);
+    flag_error(bad != 0, DL, width);
+}
+
 // ------------------------------------------------------------ filter8
 // Per-column learning filter for mid-size p (one 16-bit word per column:
 // bits 0-7 qa = ceil((lo-1) / 2^ys), bits 8-15 qb = floor(hi / 2^ys) - 1,
@@ -1032,6 +1213,33 @@ extern "C" int chp_reduce(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t
             if (!rc) rc = chp_ensure(ctx, ctx->filter, tbytes + 16);
             if (rc) return rc;
             const uint64_t ns = std::min<uint64_t>(n, std::max<uint64_t>(n / 16, 2)) & ~1ull;
+            if ((flags & CHP_REDUCE_FUSED) && !(flags & CHP_REDUCE_TMA) && ctx->coop) {
+                // One cooperative kernel (grid barriers between the phases).
+                // Opt-in: measured 433-486 vs 495 Gpts/s for three launches
+                // (its main pass spills at 64 registers).
+                if (!ctx->gridbar.p) {
+                    if ((rc = chp_ensure(ctx, ctx->gridbar, 64))) return rc;
+                    CHP_CUDA(ctx, cudaMemsetAsync(ctx->gridbar.p, 0, 64, ctx->stream));
+                }
+                const size_t smem = std::max(table_span(tbytes), kFusedMergeSmem);
+                CHP_CUDA(ctx, cudaFuncSetAttribute(k_sampled_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   (int)smem));
+                int per_sm = 0;
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sampled_fused, kThreads, smem);
+                if (per_sm >= 1) {
+                    const int init = need_init ? 1 : 0;
+                    uint16_t* scratch = (uint16_t*)ctx->sample.p;
+                    uint16_t* F = (uint16_t*)ctx->filter.p;
+                    GridBar* bar = (GridBar*)ctx->gridbar.p;
+                    void* args[] = {(void*)&d_xy, (void*)&n,     (void*)&ns, (void*)&g,   (void*)&w,   (void*)&wpad8,
+                                    (void*)&ys,   (void*)&scratch, (void*)&F, (void*)&d_L, (void*)&init, (void*)&bar};
+                    CHP_CUDA(ctx, cudaLaunchCooperativeKernel((const void*)k_sampled_fused, dim3(sblocks),
+                                                              dim3(kThreads), args, smem, ctx->stream));
+                    CHP_LAUNCHED(ctx);
+                    ctx->variant = "sampled-fused";
+                    return CHP_OK;
+                }
+            }
             CHP_CUDA(ctx, cudaFuncSetAttribute(k_sample_learn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                (int)table_span(tbytes)));
             k_sample_learn<<<sblocks, kThreads, table_span(tbytes), ctx->stream>>>(

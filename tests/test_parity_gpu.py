@@ -26,6 +26,7 @@ VARIANTS = {
     "filter8": _lib.REDUCE_FORCE_FILTER8,
     "smem16": _lib.REDUCE_FORCE_SMEM16,
     "sampled": _lib.REDUCE_FORCE_SAMPLED,
+    "sampled_fused": _lib.REDUCE_FORCE_SAMPLED | 16384,
     "smem16_tma": _lib.REDUCE_FORCE_SMEM16 | 4096,
 }
 
