@@ -86,6 +86,7 @@ uint64_t chp_dl_len(int64_t width);
 #define CHP_REDUCE_TMA 4096u        /* tuning: stream via the TMA bulk-copy ring */
 #define CHP_REDUCE_FORCE_SAMPLED 8192u /* testing: force the sampled per-column filter */
 #define CHP_REDUCE_FUSED 16384u     /* tuning: sampled filter as 1 cooperative kernel (grid barriers) */
+#define CHP_REDUCE_SAMPLE_K(k) ((uint32_t)(k) << 16) /* tuning: sample n/2^k (k in 1..7, default 4) */
 
 /* Algorithm 1 over n int32 (x,y) pairs at d_xy (8-byte aligned).  Slot of a
  * point is x - x_off - 1; a point is valid when that slot is in [0,width)

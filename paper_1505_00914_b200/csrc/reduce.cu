@@ -1212,7 +1212,10 @@ extern "C" int chp_reduce(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t
             int rc = chp_ensure(ctx, ctx->sample, (size_t)sblocks * tbytes + 16);
             if (!rc) rc = chp_ensure(ctx, ctx->filter, tbytes + 16);
             if (rc) return rc;
-            const uint64_t ns = std::min<uint64_t>(n, std::max<uint64_t>(n / 16, 2)) & ~1ull;
+            // Sample = the first n / 2^k points; k = 3 unless CHP_REDUCE_SAMPLE_K(k)
+            // (C2: k=3 510.7, k=4 505.2, k=5 474.4, k=6 430.0 Gpts/s).
+            const uint32_t kshift = (flags >> 16) & 7 ? (flags >> 16) & 7 : 3;
+            const uint64_t ns = std::min<uint64_t>(n, std::max<uint64_t>(n >> kshift, 2)) & ~1ull;
             if ((flags & CHP_REDUCE_FUSED) && !(flags & CHP_REDUCE_TMA) && ctx->coop) {
                 // One cooperative kernel (grid barriers between the phases).
                 // Opt-in: measured 433-486 vs 495 Gpts/s for three launches
