@@ -61,14 +61,28 @@ __global__ void __launch_bounds__(kCT) k_compact(const int* __restrict__ DL, uin
                                                  int2* __restrict__ lpairs, int2* __restrict__ lower,
                                                  int2* __restrict__ upper, int2* __restrict__ upperd,
                                                  long long* __restrict__ counts,
-                                                 unsigned long long* __restrict__ status, uint32_t ntiles) {
+                                                 unsigned long long* __restrict__ status,
+                                                 unsigned long long* __restrict__ status_next, uint32_t ntiles,
+                                                 int use_ticket) {
     __shared__ uint32_t s_tile;
     __shared__ unsigned long long s_warp[kCT / 32];
     __shared__ unsigned long long s_excl;
-    unsigned int* tile_counter = reinterpret_cast<unsigned int*>(status + ntiles);
-    if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
-    __syncthreads();
-    const uint32_t tile = s_tile;
+    // Tile order: block index when every tile's CTA is co-resident (no
+    // predecessor can be waiting for a slot), else an atomic ticket so that
+    // a tile only starts after all its predecessors have.
+    uint32_t tile = blockIdx.x;
+    if (use_ticket) {
+        unsigned int* tile_counter = reinterpret_cast<unsigned int*>(status + ntiles);
+        if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
+        __syncthreads();
+        tile = s_tile;
+    }
+    // The next call uses the other status array: clear it here instead of a
+    // cudaMemset before every launch.
+    if (threadIdx.x == 0) {
+        status_next[tile] = 0ull;
+        if (tile == 0) reinterpret_cast<unsigned int*>(status_next + ntiles)[0] = 0u;
+    }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t slot0 = (uint64_t)tile * kTile + (uint64_t)threadIdx.x * kItems;
     const int2* gL = reinterpret_cast<const int2*>(DL);
@@ -225,16 +239,38 @@ extern "C" int chp_compact(chp_ctx* ctx, const int32_t* d_L, int64_t width, int6
     if (width < 1 || width > (1ll << 29)) return chp_einval(ctx, "compact: width must be in [1, 2^29]");
     if (!d_counts) return chp_einval(ctx, "compact: counts buffer required");
     const uint32_t ntiles = (uint32_t)((width + kTile - 1) / kTile);
-    int rc = chp_ensure(ctx, ctx->tile_status, (size_t)ntiles * 8 + 16);
-    if (rc) return rc;
-    CHP_CUDA(ctx, cudaMemsetAsync(ctx->tile_status.p, 0, (size_t)ntiles * 8 + 16, ctx->stream));
+    // Two status arrays of (cap + 2) words, used alternately; each launch
+    // clears the other one's first ntiles entries (no memset per call).
+    const size_t need = 2 * ((size_t)ntiles + 2) * 8;
+    if (ctx->tile_status.bytes < need) {
+        int rc = chp_ensure(ctx, ctx->tile_status, need);
+        if (rc) return rc;
+        ctx->status_cap = (uint32_t)(ctx->tile_status.bytes / 16 - 2);
+        CHP_CUDA(ctx, cudaMemsetAsync(ctx->tile_status.p, 0, ctx->tile_status.bytes, ctx->stream));
+        ctx->status_clean[0] = ctx->status_clean[1] = ctx->status_cap;
+    }
+    unsigned long long* base = reinterpret_cast<unsigned long long*>(ctx->tile_status.p);
+    const int cur = ctx->status_parity;
+    unsigned long long* st_cur = base + (size_t)cur * (ctx->status_cap + 2);
+    unsigned long long* st_next = base + (size_t)(cur ^ 1) * (ctx->status_cap + 2);
+    if (ctx->status_clean[cur] < ntiles)
+        CHP_CUDA(ctx, cudaMemsetAsync(st_cur, 0, ((size_t)ctx->status_cap + 2) * 8, ctx->stream));
+    if (ctx->compact_resident == 0) {
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_compact, kCT, 0);
+        ctx->compact_resident = (uint32_t)std::max(per_sm, 1) * (uint32_t)ctx->sm_count;
+    }
+    const int use_ticket = ntiles > ctx->compact_resident ? 1 : 0;
     Map m{major_off, minor_off, swapped};
     k_compact<<<ntiles, kCT, 0, ctx->stream>>>(
         d_L, (uint32_t)width, m, reinterpret_cast<int2*>(d_chain), reinterpret_cast<unsigned long long*>(d_occ),
         reinterpret_cast<int2*>(d_Lpairs), reinterpret_cast<int2*>(d_lower), reinterpret_cast<int2*>(d_upper),
-        reinterpret_cast<int2*>(d_upperd), reinterpret_cast<long long*>(d_counts),
-        reinterpret_cast<unsigned long long*>(ctx->tile_status.p), ntiles);
+        reinterpret_cast<int2*>(d_upperd), reinterpret_cast<long long*>(d_counts), st_cur, st_next, ntiles,
+        use_ticket);
     CHP_LAUNCHED(ctx);
+    ctx->status_clean[cur] = 0;         // dirty now
+    ctx->status_clean[cur ^ 1] = ntiles;  // cleared by this launch
+    ctx->status_parity = cur ^ 1;
     return CHP_OK;
 }
 
