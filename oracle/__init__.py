@@ -155,6 +155,24 @@ class Oracle:
         self.L.or_min_max(_p(xy), len(xy), _p(out))
         return tuple(int(v) for v in out)
 
+    def precondition(self, points):
+        """reducer::precondition, x-only mode (src/reducer.cpp:235-281):
+        bounds, width = x_max - x_min + 1, bucket with x_off = x_min - 1 and
+        y untranslated, Lemma-1 chain, Melkman hull."""
+        xy = _xy(points)
+        if len(xy) == 0:
+            raise ValueError("precondition: empty input")
+        xmin, xmax, ymin, ymax = self.min_max(xy)
+        w = xmax - xmin + 1
+        lo = np.zeros(w, np.int32)
+        hi = np.zeros(w, np.int32)
+        valid = np.zeros(w, np.uint8)
+        occ = np.zeros((w + 63) // 64, np.uint64)
+        self.L.or_bucket(_p(xy), len(xy), xmin - 1, _p(lo), _p(hi), _p(valid), _p(occ))
+        arr = {"width": w, "lo": lo, "hi": hi, "valid": valid, "occ": occ}
+        chain = self.build_polyline(arr, major_off=xmin - 1)
+        return {"bbox": (xmin, xmax, ymin, ymax), "arr": arr, "chain": chain, "hull": self.melkman(chain)}
+
     def pipeline(self, points, width: int, q: int | None = None):
         """reduce -> L pairs, Lemma-1 chain, melkman hull (the reference
         pipeline of SURVEY.md section 3.3 plus section 3.1's hull)."""

@@ -175,19 +175,55 @@ def precondition(points, options: PreconditionOptions | None = None) -> Precondi
     import time
 
     options = options or PreconditionOptions()
-    if options.second_scan or options.auto_axis:
-        raise NotImplementedError("second_scan / auto_axis are the next rows of SURVEY.md 8(f)")
     xy = _as_int32_points(points)
     if len(xy) == 0:
         raise ValueError("precondition: empty input")
+    ctx = default_context()
     t0 = time.perf_counter()
-    res = default_context().precondition_host(xy, chain=True)
-    t = time.perf_counter() - t0
-    x_min, x_max, y_min, y_max = res["bbox"]
-    chain = res["chain"]
-    arr = ExtremalArray(res["L"], major_offset=x_min - 1, minor_offset=0, occ_kind=options.occ_kind, _chain=chain)
-    return PreconditionResult(arr, PolygonalChain(chain.copy()), BoundingBox(x_min, x_max, y_min, y_max),
-                              t_reduce=t)
+    x_min, x_max, y_min, y_max = ctx.precondition_host(xy, chain=False)["bbox"]
+    bbox = BoundingBox(x_min, x_max, y_min, y_max)
+    full_bounds = options.second_scan or options.auto_axis
+    swap = options.auto_axis and bbox.height() < bbox.width()  # bucket along the short side
+    t1 = time.perf_counter()
+    res = ctx.precondition_host(xy[:, ::-1].copy() if swap else xy, chain=True)
+    # Device L stores untranslated minor values; translate them when the
+    # reference does (full_bounds: src/reducer.cpp:259-261).
+    minor_off = ((x_min if swap else y_min) - 1) if full_bounds else 0
+    pairs = res["L"].astype(np.int64)
+    valid = pairs[:, 0] <= pairs[:, 1]
+    pairs[valid] -= minor_off
+    major_off = (y_min if swap else x_min) - 1
+    chain = res["chain"][:, ::-1].copy() if swap else res["chain"]
+    arr = ExtremalArray(pairs.astype(np.int32), major_offset=major_off, minor_offset=minor_off, axis_swapped=swap,
+                        occ_kind=options.occ_kind, _chain=chain)
+    t2 = time.perf_counter()
+    if options.second_scan:
+        arr = second_scan(arr, options.occ_kind)
+        chain = build_polyline(arr).vertices
+    t3 = time.perf_counter()
+    return PreconditionResult(arr, PolygonalChain(np.ascontiguousarray(chain)), bbox, t_bounds=t1 - t0,
+                              t_reduce=t2 - t1, t_extract=t3 - t2)
+
+
+def second_scan(arr: ExtremalArray, occ_kind: Kind = Kind.array) -> ExtremalArray:
+    """Re-bucket the survivors along the other axis (src/reducer.cpp:184-209):
+    the <= 2w survivors are re-reduced on the device with axes swapped."""
+    pts = arr.valid_points().astype(np.int64)
+    swapped = not arr.axis_swapped
+    if len(pts) == 0:
+        w = arr.width()
+        return ExtremalArray(np.tile(np.array([[w + 1, -1]], np.int32), (w, 1)), axis_swapped=swapped,
+                             occ_kind=occ_kind)
+    major = pts[:, 1] if swapped else pts[:, 0]
+    minor = pts[:, 0] if swapped else pts[:, 1]
+    major_min, major_max, minor_min = int(major.min()), int(major.max()), int(minor.min())
+    rebased = np.stack([major - (major_min - 1), minor - (minor_min - 1)], axis=1)
+    out = reduce(rebased, major_max - major_min + 1, None, occ_kind)
+    out.major_offset = major_min - 1
+    out.minor_offset = minor_min - 1
+    out.axis_swapped = swapped
+    out._chain = None  # the cached chain was built without these offsets
+    return out
 
 
 def translate(points, bbox: BoundingBox) -> np.ndarray:

@@ -120,20 +120,8 @@ def test_oracle_matches_reference_precondition(orc, ref):
     for _ in range(50):
         pts = mixed_case(rng, int(rng.integers(1, 500))).astype(np.int32)
         r = ref.precondition(pts)
-        xmin, xmax, ymin, ymax = orc.min_max(pts)
-        assert r["bbox"] == (xmin, xmax, ymin, ymax)
-        # precondition = reduce of x-translated points, y untranslated
-        shifted = pts.astype(np.int64)
-        shifted[:, 0] -= xmin - 1
-        arr = {"width": xmax - xmin + 1}
-        w = arr["width"]
-        lo = np.zeros(w, np.int32)
-        hi = np.zeros(w, np.int32)
-        valid = np.zeros(w, np.uint8)
-        occ = np.zeros((w + 63) // 64, np.uint64)
-        orc.L.or_bucket(np.ascontiguousarray(pts).ctypes.data, len(pts), xmin - 1, lo.ctypes.data,
-                        hi.ctypes.data, valid.ctypes.data, occ.ctypes.data)
-        arr.update(lo=lo, hi=hi, valid=valid, occ=occ)
-        chain = orc.build_polyline(arr, major_off=xmin - 1)
-        assert np.array_equal(r["chain"], chain)
-        assert np.array_equal(r["hull"], orc.melkman(chain))
+        o = orc.precondition(pts)
+        assert r["bbox"] == o["bbox"]
+        assert r["major_offset"] == o["bbox"][0] - 1 and r["minor_offset"] == 0
+        assert np.array_equal(r["chain"], o["chain"])
+        assert np.array_equal(r["hull"], o["hull"])
