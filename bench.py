@@ -210,11 +210,20 @@ def main():
     import torch.distributed as dist
 
     from paper_1505_00914_b200.device import Context
+    from paper_1505_00914_b200.shard import allreduce_dl
 
     rank, world, local = env_rank()
+    # One process per GPU over NCCL.  CHP_DIST_BACKEND=gloo (with ranks
+    # wrapped onto the visible devices) exists only to exercise the N > 1
+    # control flow on a 1-GPU box; it is not a measurement configuration.
+    backend = os.environ.get("CHP_DIST_BACKEND", "nccl")
+    local = local % max(torch.cuda.device_count(), 1)
     if world > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     n_cfg, p, seed, desc = CONFIGS[args.config]
@@ -241,7 +250,7 @@ def main():
             b.record(stream)
             k1_ev.append((a, b))
         if world > 1:
-            dist.all_reduce(DL, op=dist.ReduceOp.MIN)
+            allreduce_dl(DL)  # the path's one exchange: element-wise MIN of the partial Ls
         return ctx.compact(DL, p, chain=True, bufs=bufs)
 
     for _ in range(max(args.warmup, 3)):
