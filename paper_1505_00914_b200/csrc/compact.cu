@@ -37,13 +37,16 @@ __device__ __forceinline__ unsigned long long pack_status(unsigned long long fla
 __device__ __forceinline__ unsigned long long unpack_cv(unsigned long long st) {
     return (st & kMask31) | (((st >> 31) & kMask31) << 32);
 }
+// A status word is self-contained (flag and both counters in one 64-bit
+// access) and nothing else is published through it, so relaxed gpu-scope
+// accesses suffice; acquire loads cost an L1 invalidate (CCTL.IVALL) each.
 __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
     unsigned long long v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
 __device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 struct Map {

@@ -554,12 +554,14 @@ __global__ void __launch_bounds__(kThreads) k_reduce_filter(const int32_t* __res
 // Tables are dumped as (ua, 255 - ub) so the merge is one byte-wise min.
 // With init_dl the kernel also initialises DL (the main pass runs after it in
 // stream order), saving the separate k_dl_init launch.
+template <bool TMA>
 __global__ void __launch_bounds__(kThreads) k_sample_learn(const int32_t* __restrict__ xy, uint64_t n, Geo g,
                                                            uint32_t width, uint32_t wpad, uint32_t ys,
                                                            uint16_t* __restrict__ scratch, int* __restrict__ DL,
-                                                           int init_dl) {
+                                                           int init_dl, int stages) {
     extern __shared__ uint4 smem4[];
     uint16_t* T = reinterpret_cast<uint16_t*>(smem4);
+    uint8_t* ring = reinterpret_cast<uint8_t*>(smem4) + table_span((size_t)wpad * 2);
     for (uint32_t c = threadIdx.x; c < wpad; c += blockDim.x) T[c] = 0x00FF;  // ua = 255 > ub = 0: empty
     if (init_dl) {
         const uint64_t words = 2ull * width;
@@ -580,7 +582,7 @@ __global__ void __launch_bounds__(kThreads) k_sample_learn(const int32_t* __rest
         const uint32_t nw = ua | (ub << 8);
         if (nw != w) T[s] = (uint16_t)nw;
     };
-    for_each_point(xy, n, f);
+    stream_points<TMA>(xy, n, ring, stages, per_point4(f), f);
     __syncthreads();
     uint4* dst = reinterpret_cast<uint4*>(scratch + (size_t)blockIdx.x * wpad);
     for (uint32_t i = threadIdx.x; i < wpad / 8; i += blockDim.x) {
@@ -1243,11 +1245,14 @@ extern "C" int chp_reduce(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t
                     return CHP_OK;
                 }
             }
-            CHP_CUDA(ctx, cudaFuncSetAttribute(k_sample_learn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)table_span(tbytes)));
-            k_sample_learn<<<sblocks, kThreads, table_span(tbytes), ctx->stream>>>(
-                d_xy, ns, g, w, wpad8, ys, (uint16_t*)ctx->sample.p, d_L, need_init ? 1 : 0);
-            CHP_LAUNCHED(ctx);
+            {
+                const Plan sp = plan_for(ctx, tbytes, (flags & CHP_REDUCE_SAMPLE_TMA) ? CHP_REDUCE_TMA : 0u, false);
+                auto fn = sp.tma ? k_sample_learn<true> : k_sample_learn<false>;
+                CHP_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp.smem));
+                fn<<<sblocks, kThreads, sp.smem, ctx->stream>>>(d_xy, ns, g, w, wpad8, ys, (uint16_t*)ctx->sample.p,
+                                                                d_L, need_init ? 1 : 0, sp.stages);
+                CHP_LAUNCHED(ctx);
+            }
             const uint32_t nchunks = wpad8 / 8;
             k_sample_merge<<<(nchunks + kMergeCols - 1) / kMergeCols, dim3(kMergeCols, kMergeSlices), 0,
                              ctx->stream>>>((const uint16_t*)ctx->sample.p, sblocks, w, wpad8,
