@@ -66,6 +66,19 @@ __device__ __forceinline__ bool accept(const Geo& g, int32_t x, int32_t y, uint3
     return ok;
 }
 
+// An opaque copy: the value must live in a register from here on, so the
+// compiler cannot rematerialise it (uniform-datapath S2UR/LDCU) per use.
+__device__ __forceinline__ uint32_t pin(uint32_t v) {
+    asm volatile("" : "+r"(v));
+    return v;
+}
+
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+
 __device__ __forceinline__ void flag_error(bool bad, int* DL, uint32_t width) {
     if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) red_min(DL + 2ull * width, -1);
 }
@@ -310,51 +323,57 @@ __global__ void __launch_bounds__(kThreads) k_reduce_smem32(const int32_t* __res
 }
 
 // ------------------------------------------------------------ smem16
-// Slot word: bits 0-15 a = y - ybase (min), bits 16-31 b = 0xFFFF - a (min).
-template <bool VALIDATE, bool TMA>
+// Slot word: bits 0-15 a = y - 1 (min), bits 16-31 b = 0xFFFF - a (min);
+// empty = 0xFFFFFFFF.  Only for validated input with 1 <= y <= q <= 65536,
+// so a = y - 1 always fits 16 bits and the point's own word is
+//   pw = a | (0xFFFF - a) << 16 = 0xFFFF0000 - a * 0xFFFF.
+// A point changes its slot iff vminu2(w, pw) != w (one VIMNMX.U16x2).  The
+// hit path is branch-free with the shared base hoisted: the branchy form
+// issued ~27 instructions per point (per-point S2UR of the shared window,
+// three branches) and ran issue-bound (ncu C3: 79% issue-active).
+template <bool TMA>
 __global__ void __launch_bounds__(kThreads) k_reduce_smem16(const int32_t* __restrict__ xy, uint64_t n,
-                                                            Geo g, uint32_t width, int32_t ybase, int stages,
+                                                            Geo g, uint32_t width, int stages,
                                                             int* __restrict__ DL) {
     extern __shared__ uint4 smem4[];
     uint32_t* sW = reinterpret_cast<uint32_t*>(smem4);
     uint8_t* ring = reinterpret_cast<uint8_t*>(smem4) + table_span((size_t)width * 4);
     for (uint32_t c = threadIdx.x; c < width; c += blockDim.x) sW[c] = 0xFFFFFFFFu;
     __syncthreads();
-    bool bad = false;
-    auto f = [&](int32_t x, int32_t y) {
-        uint32_t s;
-        if (!accept<VALIDATE>(g, x, y, s)) {
-            bad = true;
-            return;
-        }
-        const uint32_t a = (uint32_t)y - (uint32_t)ybase;
-        if (a > 0xFFFFu) {  // outside the packed window: straight to L2
-            red_min(DL + 2ull * s, y);
-            red_min(DL + 2ull * s + 1, ~y);
-            return;
-        }
-        const uint32_t b = 0xFFFFu - a;
-        uint32_t w = sW[s];
-        if (a < (w & 0xFFFFu) || b < (w >> 16)) {
+    // Kernel constants pinned in ordinary registers: left to the compiler,
+    // the shared window base (S2UR + ULEA) and the Geo words (LDCU) are
+    // rematerialised for every point.
+    const uint32_t tbase = pin((uint32_t)__cvta_generic_to_shared(smem4));
+    const uint32_t base = pin(g.base), wcheck = pin(g.wcheck), qmax = pin(g.qmax);
+    uint32_t bad = 0;
+    auto one = [&](int32_t x, int32_t y) {
+        uint32_t s = slot_of(x, base);
+        const uint32_t ym1 = (uint32_t)y - 1u;
+        const bool ok = (s < wcheck) & (ym1 < qmax);
+        bad |= !ok;
+        s = ok ? s : 0u;
+        const uint32_t pw = 0xFFFF0000u - ym1 * 0xFFFFu;
+        uint32_t w = lds_u32(tbase + 4 * s);
+        if (ok & (__vminu2(w, pw) != w)) {  // rare: the point moves an extreme
             for (;;) {
-                const uint32_t nw = min(w & 0xFFFFu, a) | (min(w >> 16, b) << 16);
+                const uint32_t nw = __vminu2(w, pw);
                 if (nw == w) break;
-                const uint32_t old = atomicCAS(&sW[s], w, nw);
+                const uint32_t old = atomicCAS(sW + s, w, nw);
                 if (old == w) break;
                 w = old;
             }
         }
     };
-    stream_points<TMA>(xy, n, ring, stages, per_point4(f), f);
-    flag_error(bad, DL, width);
+    stream_points<TMA>(xy, n, ring, stages, per_point4(one), one);
+    flag_error(bad != 0, DL, width);
     __syncthreads();
     int2* __restrict__ gL = reinterpret_cast<int2*>(DL);
     for (uint32_t c = threadIdx.x; c < width; c += blockDim.x) {
         const uint32_t w = sW[c];
         const uint32_t a = w & 0xFFFFu, b = w >> 16;
         if (a > 0xFFFFu - b) continue;  // lo > hi: empty
-        const int32_t lo = ybase + (int32_t)a;
-        const int32_t nhi = ~(ybase + (int32_t)(0xFFFFu - b));
+        const int32_t lo = 1 + (int32_t)a;
+        const int32_t nhi = ~(1 + (int32_t)(0xFFFFu - b));
         const int2 cur = ld_cg2(gL + c);
         if (lo < cur.x) red_min(DL + 2ull * c, lo);
         if (nhi < cur.y) red_min(DL + 2ull * c + 1, nhi);
@@ -1176,12 +1195,10 @@ extern "C" int chp_reduce(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t
         }
         case V_SMEM16: {
             const Plan pl = plan_for(ctx, (size_t)w * 4, flags, false);
-            if (validate)
-                CHP_LAUNCH_PLANNED(ctx, pl, (k_reduce_smem16<true, true>), (k_reduce_smem16<true, false>), d_xy, n,
-                                   g, w, 1, pl.stages, d_L);
-            else
-                CHP_LAUNCH_PLANNED(ctx, pl, (k_reduce_smem16<false, true>), (k_reduce_smem16<false, false>), d_xy,
-                                   n, g, w, 1, pl.stages, d_L);
+            // fits16 implies validation with 1 <= y <= q <= 65536 (the kernel's
+            // packed window).
+            CHP_LAUNCH_PLANNED(ctx, pl, k_reduce_smem16<true>, k_reduce_smem16<false>, d_xy, n, g, w, pl.stages,
+                               d_L);
             ctx->variant = pl.tma ? "smem16+tma" : "smem16";
             return CHP_OK;
         }
