@@ -694,11 +694,17 @@ __global__ void __launch_bounds__(kThreads) k_reduce_sampled(const int32_t* __re
     uint32_t bad = 0;
     // Rare path: a point outside the strict interior of its column.  Inlined
     // (an out-of-line __noinline__ version measured 411 vs 491 Gpts/s).
+    // Validation lives here too: an invalid point always reaches it (below).
     auto settle = [&](uint32_t s, int32_t y) {
+        const uint32_t ym1 = (uint32_t)y - 1u;
+        if (s >= g.wcheck || ym1 >= g.qmax) {
+            bad = 1;
+            return;
+        }
         const uint32_t a = tbase + 2 * s;
         const uint32_t w = lds_u16(a);
         const uint32_t lo = w & 0xFFu, span = w >> 8;
-        const uint32_t u = ((uint32_t)y - 1u) >> ys;
+        const uint32_t u = ym1 >> ys;
         if (span == 0) {  // nothing known: both sides may move
             red_min(DL + 2ull * s, y);
             red_min(DL + 2ull * s + 1, ~y);
@@ -712,16 +718,17 @@ __global__ void __launch_bounds__(kThreads) k_reduce_sampled(const int32_t* __re
             if (u > lo + span) sts_u16(a, lo | ((u - lo) << 8));
         }
     };
-    // Branch-free hit test of one point: returns true when it must be settled.
+    // Hit test of one point, branch-free: true when it must be settled.  An
+    // invalid x clamps to slot `width`, whose word (span 0) never skips (the
+    // host guarantees wcheck == width and a table of at least width + 1
+    // slots); an invalid y has (y - 1) >> ys >= every ub of a strict
+    // interior (or wraps), so it misses too.  Validation thus costs one
+    // IMNMX per point instead of two compares, a select and a flag.
     auto test = [&](int32_t x, int32_t y, uint32_t& s) -> bool {
-        s = slot_of(x, g.base);
-        const uint32_t ym1 = (uint32_t)y - 1u;
-        const bool ok = (s < g.wcheck) & (ym1 < g.qmax);
-        bad |= !ok;
-        s = ok ? s : 0u;
+        s = min(slot_of(x, g.base), width);
         const uint32_t w = lds_u16(tbase + 2 * s);
         const uint32_t lo = w & 0xFFu, span = w >> 8;
-        return ok & ((ym1 >> ys) - lo >= span);  // not strictly inside
+        return (((uint32_t)y - 1u) >> ys) - lo >= span;  // not strictly inside
     };
     auto one = [&](int32_t x, int32_t y) {
         uint32_t s;
@@ -1147,8 +1154,8 @@ extern "C" int chp_reduce(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t
     const bool yknown = validate && q >= 1;  // every accepted y is in [1, q]
     const bool fits_f8 = yknown && (size_t)((w + 7) & ~7u) * 2 <= budget;
 
-    const uint32_t wpad8 = (w + 7) & ~7u;
-    const bool fits_sampled = yknown && (size_t)wpad8 * 2 <= budget;
+    const uint32_t wpad8 = (w + 8) & ~7u;  // >= w + 1: slot w is the invalid-x sink
+    const bool fits_sampled = yknown && g.wcheck == w && (size_t)wpad8 * 2 <= budget;
 
     enum { V_GLOBAL, V_SMEM32, V_SMEM16, V_FILTER8, V_FILTER, V_SAMPLED } v;
     if (flags & CHP_REDUCE_FORCE_GLOBAL) v = V_GLOBAL;
