@@ -573,40 +573,76 @@ __global__ void __launch_bounds__(kThreads) k_reduce_filter(const int32_t* __res
 // Tables are dumped as (ua, 255 - ub) so the merge is one byte-wise min.
 // With init_dl the kernel also initialises DL (the main pass runs after it in
 // stream order), saving the separate k_dl_init launch.
-template <bool TMA>
-__global__ void __launch_bounds__(kThreads) k_sample_learn(const int32_t* __restrict__ xy, uint64_t n, Geo g,
-                                                           uint32_t width, uint32_t wpad, uint32_t ys,
-                                                           uint16_t* __restrict__ scratch, int* __restrict__ DL,
-                                                           int init_dl, int stages) {
-    extern __shared__ uint4 smem4[];
-    uint16_t* T = reinterpret_cast<uint16_t*>(smem4);
-    uint8_t* ring = reinterpret_cast<uint8_t*>(smem4) + table_span((size_t)wpad * 2);
-    for (uint32_t c = threadIdx.x; c < wpad; c += blockDim.x) T[c] = 0x00FF;  // ua = 255 > ub = 0: empty
+// Phase helpers shared by the three-launch pipeline and the fused kernel.
+__device__ __forceinline__ void sample_init(uint4* smem4, uint32_t wpad, int* __restrict__ DL, uint32_t width,
+                                            int init_dl) {
+    for (uint32_t c = threadIdx.x; c < wpad / 8; c += blockDim.x)  // ua = 255 > ub = 0: empty
+        smem4[c] = make_uint4(0x00FF00FFu, 0x00FF00FFu, 0x00FF00FFu, 0x00FF00FFu);
     if (init_dl) {
         const uint64_t words = 2ull * width;
-        for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < words; i += (uint64_t)gridDim.x * blockDim.x)
+        for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < words;
+             i += (uint64_t)gridDim.x * blockDim.x)
             DL[i] = CHP_EMPTY;
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             DL[words] = 0;
             DL[words + 1] = 0;
         }
     }
-    __syncthreads();
+}
+
+// Fold this CTA's share of the sample into T.  No validation here: an
+// invalid x lands in the sink slot `width` (never merged), an invalid y can
+// only garble its own column's word, and the main pass, which sees every
+// point again, fails the call.
+template <bool TMA>
+__device__ __forceinline__ void sample_fold(const int32_t* __restrict__ xy, uint64_t n, const Geo& g,
+                                            uint32_t width, uint32_t ys, uint16_t* T, uint8_t* ring, int stages) {
     auto f = [&](int32_t x, int32_t y) {
-        uint32_t s;
-        if (!accept<true>(g, x, y, s)) return;  // the main pass flags it
+        const uint32_t s = min(slot_of(x, g.base), width);
         const uint32_t u = ((uint32_t)y - 1u) >> ys;
         const uint32_t w = T[s];
-        const uint32_t ua = min(w & 0xFFu, u), ub = max(w >> 8, u);
-        const uint32_t nw = ua | (ub << 8);
+        const uint32_t nw = min(w & 0xFFu, u) | (max(w >> 8, u) << 8);
         if (nw != w) T[s] = (uint16_t)nw;
     };
-    stream_points<TMA>(xy, n, ring, stages, per_point4(f), f);
-    __syncthreads();
+    if (TMA) {
+        stream_points<true>(xy, n, ring, stages, per_point4(f), f);
+        return;
+    }
+    // Each thread sees only ~80 sample points, so the pass is bound by
+    // round trips, not bandwidth: 8 vectors per thread in flight at once
+    // (5 round trips instead of 10 for the C2 sample).
+    const Split sp = split_points(xy, n);
+    const int4* __restrict__ v = reinterpret_cast<const int4*>(xy + 2 * sp.head);
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + 7 * stride < sp.nvec; i += 8 * stride) {
+        int4 q[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) q[j] = ld_stream(v + i + j * stride);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            f(q[j].x, q[j].y);
+            f(q[j].z, q[j].w);
+        }
+    }
+    for (; i < sp.nvec; i += stride) {
+        const int4 a = ld_stream(v + i);
+        f(a.x, a.y);
+        f(a.z, a.w);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (sp.head) f(xy[0], xy[1]);
+        if (sp.tail) f(xy[2 * (n - 1)], xy[2 * (n - 1) + 1]);
+    }
+}
+
+// This CTA's table to scratch as (ua, 255 - ub), so the merge is one
+// byte-wise min.
+__device__ __forceinline__ void sample_dump(const uint4* smem4, uint16_t* __restrict__ scratch, uint32_t wpad) {
     uint4* dst = reinterpret_cast<uint4*>(scratch + (size_t)blockIdx.x * wpad);
     for (uint32_t i = threadIdx.x; i < wpad / 8; i += blockDim.x) {
         uint4 q = smem4[i];
-        q.x ^= 0xFF00FF00u;  // ub -> 255 - ub in the high byte of each word
+        q.x ^= 0xFF00FF00u;
         q.y ^= 0xFF00FF00u;
         q.z ^= 0xFF00FF00u;
         q.w ^= 0xFF00FF00u;
@@ -614,39 +650,17 @@ __global__ void __launch_bounds__(kThreads) k_sample_learn(const int32_t* __rest
     }
 }
 
-// Byte-wise min over the CTA tables: thread (x, y) folds tables y, y+8, ...
-// for 8 columns (one uint4), then the 8 partials meet in shared memory.
-constexpr int kMergeCols = 16;   // uint4 chunks per block (x)
-constexpr int kMergeSlices = 16; // table slices per block (y): ~10 loads in flight per thread
+__device__ __forceinline__ void vmin4x4(uint4& m, const uint4& q) {
+    m.x = __vminu4(m.x, q.x);
+    m.y = __vminu4(m.y, q.y);
+    m.z = __vminu4(m.z, q.z);
+    m.w = __vminu4(m.w, q.w);
+}
 
-__global__ void __launch_bounds__(kMergeCols * kMergeSlices) k_sample_merge(const uint16_t* __restrict__ scratch,
-                                                                           uint32_t ntables, uint32_t width,
-                                                                           uint32_t wpad, uint16_t* __restrict__ F) {
-    __shared__ uint4 part[kMergeSlices][kMergeCols];
-    const uint32_t chunk = blockIdx.x * kMergeCols + threadIdx.x;
-    const uint32_t nchunks = wpad / 8;
-    uint4 m = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
-    if (chunk < nchunks) {
-        const uint4* src = reinterpret_cast<const uint4*>(scratch) + chunk;
-#pragma unroll 5
-        for (uint32_t t = threadIdx.y; t < ntables; t += kMergeSlices) {
-            const uint4 q = __ldcs(src + (size_t)t * nchunks);
-            m.x = __vminu4(m.x, q.x);
-            m.y = __vminu4(m.y, q.y);
-            m.z = __vminu4(m.z, q.z);
-            m.w = __vminu4(m.w, q.w);
-        }
-    }
-    part[threadIdx.y][threadIdx.x] = m;
-    __syncthreads();
-    if (threadIdx.y != 0 || chunk >= nchunks) return;
-    for (int k = 1; k < kMergeSlices; ++k) {
-        const uint4 q = part[k][threadIdx.x];
-        m.x = __vminu4(m.x, q.x);
-        m.y = __vminu4(m.y, q.y);
-        m.z = __vminu4(m.z, q.z);
-        m.w = __vminu4(m.w, q.w);
-    }
+// Merged (ua, 255 - ub) bytes of 8 columns -> 8 main-pass words: the strict
+// interior lo = ua + 1, span = ub - lo; columns >= width (incl. the sink) and
+// empty columns get lo = 255, span = 0 (never skip).
+__device__ __forceinline__ uint4 interior_words(const uint4& m, uint32_t chunk, uint32_t width) {
     const uint32_t words[4] = {m.x, m.y, m.z, m.w};
     uint32_t out[4];
 #pragma unroll
@@ -657,7 +671,7 @@ __global__ void __launch_bounds__(kMergeCols * kMergeSlices) k_sample_merge(cons
             const uint32_t c = chunk * 8 + k * 2 + h;
             const uint32_t w16 = (words[k] >> (16 * h)) & 0xFFFFu;
             const uint32_t ua = w16 & 0xFFu, ub = 255u - (w16 >> 8);
-            uint32_t word = 0x00FF;  // lo = 255, span = 0: never skip
+            uint32_t word = 0x00FF;
             if (c < width && ua <= ub) {
                 const uint32_t lo = ua + 1;  // <= 255 because buckets stop at 254
                 word = lo | ((ub > lo ? ub - lo : 0) << 8);
@@ -666,7 +680,56 @@ __global__ void __launch_bounds__(kMergeCols * kMergeSlices) k_sample_merge(cons
         }
         out[k] = o;
     }
-    reinterpret_cast<uint4*>(F)[chunk] = make_uint4(out[0], out[1], out[2], out[3]);
+    return make_uint4(out[0], out[1], out[2], out[3]);
+}
+
+template <bool TMA>
+__global__ void __launch_bounds__(kThreads) k_sample_learn(const int32_t* __restrict__ xy, uint64_t n, Geo g,
+                                                           uint32_t width, uint32_t wpad, uint32_t ys,
+                                                           uint16_t* __restrict__ scratch, int* __restrict__ DL,
+                                                           int init_dl, int stages) {
+    extern __shared__ uint4 smem4[];
+    uint8_t* ring = reinterpret_cast<uint8_t*>(smem4) + table_span((size_t)wpad * 2);
+    sample_init(smem4, wpad, DL, width, init_dl);
+    __syncthreads();
+    sample_fold<TMA>(xy, n, g, width, ys, reinterpret_cast<uint16_t*>(smem4), ring, stages);
+    __syncthreads();
+    sample_dump(smem4, scratch, wpad);
+}
+
+// Byte-wise min over the CTA tables: thread (x, y) folds tables y, y+16, ...
+// for 8 columns (one uint4) with all its loads in flight at once (a single
+// round trip for <= 160 tables), then the 16 partials meet in shared memory.
+constexpr int kMergeCols = 16;    // uint4 chunks per block (x)
+constexpr int kMergeSlices = 16;  // table slices per block (y)
+constexpr int kMergeBatch = 10;   // loads in flight per thread
+
+__global__ void __launch_bounds__(kMergeCols * kMergeSlices) k_sample_merge(const uint16_t* __restrict__ scratch,
+                                                                           uint32_t ntables, uint32_t width,
+                                                                           uint32_t wpad, uint16_t* __restrict__ F) {
+    __shared__ uint4 part[kMergeSlices][kMergeCols];
+    const uint32_t chunk = blockIdx.x * kMergeCols + threadIdx.x;
+    const uint32_t nchunks = wpad / 8;
+    const uint4 ones = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+    uint4 m = ones;
+    if (chunk < nchunks) {
+        const uint4* src = reinterpret_cast<const uint4*>(scratch) + chunk;
+        for (uint32_t t0 = threadIdx.y; t0 < ntables; t0 += kMergeSlices * kMergeBatch) {
+            uint4 q[kMergeBatch];
+#pragma unroll
+            for (int k = 0; k < kMergeBatch; ++k) {
+                const uint32_t t = t0 + k * kMergeSlices;
+                q[k] = t < ntables ? __ldcs(src + (size_t)t * nchunks) : ones;
+            }
+#pragma unroll
+            for (int k = 0; k < kMergeBatch; ++k) vmin4x4(m, q[k]);
+        }
+    }
+    part[threadIdx.y][threadIdx.x] = m;
+    __syncthreads();
+    if (threadIdx.y != 0 || chunk >= nchunks) return;
+    for (int k = 1; k < kMergeSlices; ++k) vmin4x4(m, part[k][threadIdx.x]);
+    reinterpret_cast<uint4*>(F)[chunk] = interior_words(m, chunk, width);
 }
 
 __device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
@@ -678,19 +741,12 @@ __device__ __forceinline__ void sts_u16(uint32_t addr, uint32_t v) {
     asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"((uint16_t)v) : "memory");
 }
 
+// The main pass over all n points against the strict-interior table at
+// shared address tbase (>= width + 1 words; word `width` never skips).
 template <bool TMA>
-__global__ void __launch_bounds__(kThreads) k_reduce_sampled(const int32_t* __restrict__ xy, uint64_t n, Geo g,
-                                                             uint32_t width, uint32_t wpad, uint32_t ys,
-                                                             const uint16_t* __restrict__ F, int stages,
-                                                             int* __restrict__ DL) {
-    extern __shared__ uint4 smem4[];
-    uint8_t* ring = reinterpret_cast<uint8_t*>(smem4) + table_span((size_t)wpad * 2);
-    {
-        const uint4* F4 = reinterpret_cast<const uint4*>(F);
-        for (uint32_t i = threadIdx.x; i < wpad / 8; i += blockDim.x) smem4[i] = __ldcg(F4 + i);
-    }
-    __syncthreads();
-    const uint32_t tbase = (uint32_t)__cvta_generic_to_shared(smem4);  // hoisted shared base
+__device__ __forceinline__ void sampled_pass(const int32_t* __restrict__ xy, uint64_t n, const Geo& g,
+                                             uint32_t width, uint32_t ys, uint32_t tbase, uint8_t* ring,
+                                             int stages, int* __restrict__ DL) {
     uint32_t bad = 0;
     // Rare path: a point outside the strict interior of its column.  Inlined
     // (an out-of-line __noinline__ version measured 411 vs 491 Gpts/s).
@@ -723,7 +779,7 @@ __global__ void __launch_bounds__(kThreads) k_reduce_sampled(const int32_t* __re
     // host guarantees wcheck == width and a table of at least width + 1
     // slots); an invalid y has (y - 1) >> ys >= every ub of a strict
     // interior (or wraps), so it misses too.  Validation thus costs one
-    // IMNMX per point instead of two compares, a select and a flag.
+    // VIADDMNMX per point instead of two compares, a select and a flag.
     auto test = [&](int32_t x, int32_t y, uint32_t& s) -> bool {
         s = min(slot_of(x, g.base), width);
         const uint32_t w = lds_u16(tbase + 2 * s);
@@ -763,6 +819,21 @@ __global__ void __launch_bounds__(kThreads) k_reduce_sampled(const int32_t* __re
     flag_error(bad != 0, DL, width);
 }
 
+template <bool TMA>
+__global__ void __launch_bounds__(kThreads) k_reduce_sampled(const int32_t* __restrict__ xy, uint64_t n, Geo g,
+                                                             uint32_t width, uint32_t wpad, uint32_t ys,
+                                                             const uint16_t* __restrict__ F, int stages,
+                                                             int* __restrict__ DL) {
+    extern __shared__ uint4 smem4[];
+    uint8_t* ring = reinterpret_cast<uint8_t*>(smem4) + table_span((size_t)wpad * 2);
+    {
+        const uint4* F4 = reinterpret_cast<const uint4*>(F);
+        for (uint32_t i = threadIdx.x; i < wpad / 8; i += blockDim.x) smem4[i] = __ldcg(F4 + i);
+    }
+    __syncthreads();
+    sampled_pass<TMA>(xy, n, g, width, ys, (uint32_t)__cvta_generic_to_shared(smem4), ring, stages, DL);
+}
+
 // ------------------------------------------------------- sampled, fused
 // The sampled pipeline as ONE cooperative kernel (all CTAs co-resident, one
 // per SM): sample pass -> grid barrier -> merge, each CTA owning 1/grid of
@@ -773,9 +844,6 @@ struct GridBar {
     unsigned count;
     unsigned gen;
 };
-
-__device__ __noinline__ void sampled_main_pass(const int32_t* __restrict__ xy, uint64_t n, Geo g, uint32_t width,
-                                               uint32_t ys, uint32_t tbase, int* __restrict__ DL);
 
 constexpr size_t kFusedMergeSmem = 16 * 64 * sizeof(uint4);  // phase B partials
 
@@ -797,97 +865,53 @@ __device__ __forceinline__ void grid_barrier(GridBar* b) {
     __syncthreads();
 }
 
+// Out of line so phases A-C do not constrain the main pass's registers.
+__device__ __noinline__ void sampled_main_pass(const int32_t* __restrict__ xy, uint64_t n, Geo g, uint32_t width,
+                                               uint32_t ys, uint32_t tbase, int* __restrict__ DL) {
+    sampled_pass<false>(xy, n, g, width, ys, tbase, nullptr, 0, DL);
+}
+
 __global__ void __launch_bounds__(kThreads) k_sampled_fused(const int32_t* __restrict__ xy, uint64_t n, uint64_t ns,
                                                             Geo g, uint32_t width, uint32_t wpad, uint32_t ys,
                                                             uint16_t* __restrict__ scratch, uint16_t* __restrict__ F,
                                                             int* __restrict__ DL, int init_dl, GridBar* bar) {
     extern __shared__ uint4 smem4[];
-    uint16_t* T = reinterpret_cast<uint16_t*>(smem4);
     const uint32_t nchunks = wpad / 8;
-    // ---- A: sample pass (as k_sample_learn) + DL init
-    for (uint32_t c = threadIdx.x; c < wpad; c += blockDim.x) T[c] = 0x00FF;
-    if (init_dl) {
-        const uint64_t words = 2ull * width;
-        for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < words;
-             i += (uint64_t)gridDim.x * blockDim.x)
-            DL[i] = CHP_EMPTY;
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
-            DL[words] = 0;
-            DL[words + 1] = 0;
-        }
-    }
+    // ---- A: sample pass + DL init
+    sample_init(smem4, wpad, DL, width, init_dl);
     __syncthreads();
-    for_each_point(xy, ns, [&](int32_t x, int32_t y) {
-        uint32_t s;
-        if (!accept<true>(g, x, y, s)) return;
-        const uint32_t u = ((uint32_t)y - 1u) >> ys;
-        const uint32_t w = T[s];
-        const uint32_t nw = min(w & 0xFFu, u) | (max(w >> 8, u) << 8);
-        if (nw != w) T[s] = (uint16_t)nw;
-    });
+    sample_fold<false>(xy, ns, g, width, ys, reinterpret_cast<uint16_t*>(smem4), nullptr, 0);
     __syncthreads();
-    {
-        uint4* dst = reinterpret_cast<uint4*>(scratch) + (size_t)blockIdx.x * nchunks;
-        for (uint32_t i = threadIdx.x; i < nchunks; i += blockDim.x) {
-            uint4 q = smem4[i];
-            q.x ^= 0xFF00FF00u;
-            q.y ^= 0xFF00FF00u;
-            q.z ^= 0xFF00FF00u;
-            q.w ^= 0xFF00FF00u;
-            dst[i] = q;
-        }
-    }
+    sample_dump(smem4, scratch, wpad);
     grid_barrier(bar);
     // ---- B: merge; this CTA owns chunks [c0, c1), 64 chunks x 16 slices
     {
         const uint32_t per = (nchunks + gridDim.x - 1) / gridDim.x;
         const uint32_t c0 = blockIdx.x * per, c1 = min(nchunks, c0 + per);
         uint4* part = smem4;  // [16][64] uint4, the table is reloaded in C
+        const uint4 ones = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
         for (uint32_t base = c0; base < c1; base += 64) {
             const uint32_t cl = threadIdx.x & 63, slice = threadIdx.x >> 6;
             const uint32_t chunk = base + cl;
-            uint4 m = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+            uint4 m = ones;
             if (chunk < c1) {
                 const uint4* src = reinterpret_cast<const uint4*>(scratch) + chunk;
-#pragma unroll 5
-                for (uint32_t t = slice; t < gridDim.x; t += 16) {
-                    const uint4 q = __ldcg(src + (size_t)t * nchunks);
-                    m.x = __vminu4(m.x, q.x);
-                    m.y = __vminu4(m.y, q.y);
-                    m.z = __vminu4(m.z, q.z);
-                    m.w = __vminu4(m.w, q.w);
+                for (uint32_t t0 = slice; t0 < gridDim.x; t0 += 16 * kMergeBatch) {
+                    uint4 q[kMergeBatch];
+#pragma unroll
+                    for (int k = 0; k < kMergeBatch; ++k) {
+                        const uint32_t t = t0 + k * 16;
+                        q[k] = t < gridDim.x ? __ldcg(src + (size_t)t * nchunks) : ones;
+                    }
+#pragma unroll
+                    for (int k = 0; k < kMergeBatch; ++k) vmin4x4(m, q[k]);
                 }
             }
             part[slice * 64 + cl] = m;
             __syncthreads();
             if (slice == 0 && chunk < c1) {
-                for (int k = 1; k < 16; ++k) {
-                    const uint4 q = part[k * 64 + cl];
-                    m.x = __vminu4(m.x, q.x);
-                    m.y = __vminu4(m.y, q.y);
-                    m.z = __vminu4(m.z, q.z);
-                    m.w = __vminu4(m.w, q.w);
-                }
-                const uint32_t words[4] = {m.x, m.y, m.z, m.w};
-                uint32_t out[4];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    uint32_t o = 0;
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const uint32_t c = chunk * 8 + k * 2 + h;
-                        const uint32_t w16 = (words[k] >> (16 * h)) & 0xFFFFu;
-                        const uint32_t ua = w16 & 0xFFu, ub = 255u - (w16 >> 8);
-                        uint32_t word = 0x00FF;
-                        if (c < width && ua <= ub) {
-                            const uint32_t lo = ua + 1;
-                            word = lo | ((ub > lo ? ub - lo : 0) << 8);
-                        }
-                        o |= word << (16 * h);
-                    }
-                    out[k] = o;
-                }
-                reinterpret_cast<uint4*>(F)[chunk] = make_uint4(out[0], out[1], out[2], out[3]);
+                for (int k = 1; k < 16; ++k) vmin4x4(m, part[k * 64 + cl]);
+                reinterpret_cast<uint4*>(F)[chunk] = interior_words(m, chunk, width);
             }
             __syncthreads();
         }
@@ -899,50 +923,10 @@ __global__ void __launch_bounds__(kThreads) k_sampled_fused(const int32_t* __res
         for (uint32_t i = threadIdx.x; i < nchunks; i += blockDim.x) smem4[i] = __ldcg(F4 + i);
     }
     __syncthreads();
-    // ---- D: main pass (as k_reduce_sampled)
+    // ---- D: main pass
     sampled_main_pass(xy, n, g, width, ys, (uint32_t)__cvta_generic_to_shared(smem4), DL);
 }
 
-// Phase D of k_sampled_fused, out of line (called once per CTA) so the hot
-// loop gets a register allocation of its own.
-__device__ __noinline__ void sampled_main_pass(const int32_t* __restrict__ xy, uint64_t n, Geo g, uint32_t width,
-                                               uint32_t ys, uint32_t tbase, int* __restrict__ DL) {
-    uint32_t bad = 0;
-    auto one = [&](int32_t x, int32_t y) {
-        const uint32_t s0 = slot_of(x, g.base);
-        const uint32_t ym1 = (uint32_t)y - 1u;
-        const bool ok = (s0 < g.wcheck) & (ym1 < g.qmax);
-        bad |= !ok;
-        const uint32_t s = ok ? s0 : 0u;
-        const uint32_t a = tbase + 2 * s;
-        const uint32_t w = lds_u16(a);
-        const uint32_t lo = w & 0xFFu, span = w >> 8;
-        const uint32_t u = ym1 >> ys;
-        if (!ok || u - lo < span) return;
-        if (span == 0) {
-            red_min(DL + 2ull * s, y);
-            red_min(DL + 2ull * s + 1, ~y);
-            return;
-        }
-        if (u < lo) {
-            red_min(DL + 2ull * s, y);
-            if (u + 1 < lo) sts_u16(a, (u + 1) | ((lo + span - u - 1) << 8));
-        } else {
-            red_min(DL + 2ull * s + 1, ~y);
-            if (u > lo + span) sts_u16(a, lo | ((u - lo) << 8));
-        }
-    };
-    for_each_group_pp(
-        xy, n,
-        [&](const int4& a, const int4& b, const int4& c, const int4& d) {
-            one(a.x, a.y); one(a.z, a.w);
-            one(b.x, b.y); one(b.z, b.w);
-            one(c.x, c.y); one(c.z, c.w);
-            one(d.x, d.y); one(d.z, d.w);
-        },
-        one);
-    flag_error(bad != 0, DL, width);
-}
 
 // ------------------------------------------------------------ filter8
 // Per-column learning filter for mid-size p (one 16-bit word per column:
