@@ -420,136 +420,163 @@ __global__ void __launch_bounds__(kThreads) k_reduce_global(const int32_t* __res
 
 // ------------------------------------------------------------ filter
 // Filter word per group of 2^gshift columns, two H-bit halves (H = 8 in a
-// 16-bit word, or 16 in a 32-bit word): low half fa, high half fb with
-//   fa = ceil((max_lo - ybase) / 2^ys),  fb = floor((min_hi - ybase + 1) / 2^ys) - 1,
-// and a point is skipped iff fa <= u <= fb for u = (y - ybase) >> ys, which
-// implies max_lo <= y <= min_hi ("filter").  Empty / unusable
-// groups are fa = all-ones, fb = 0 (never skip).
+// 16-bit word, or 16 in a 32-bit word): low half fa, high half span with
+//   fa = ceil((max_lo - 1) / 2^ys),  fb = floor(min_hi / 2^ys) - 1,
+//   span = min(fb - fa + 1, 2^H - 1)  (0 = never skip),
+// and a point is skipped iff (u - fa) < span (unsigned) for u = (y - 1) >> ys,
+// i.e. fa <= u <= fb, which implies max_lo <= y <= min_hi (DESIGN.md,
+// "filter").  The table has ngroups + 1 words: word ngroups is the sink of
+// invalid x (x clamps to slot `width`), and a partial last group is "never"
+// too, so the clamp can only land on a never-skip word.
 template <typename W>
 struct FW {
     static constexpr uint32_t kHalf = sizeof(W) * 4;
     static constexpr uint32_t kMask = (1u << kHalf) - 1u;
-    static constexpr W kNever = (W)kMask;
+    static constexpr W kNever = (W)0;  // span 0
 };
 
 template <typename W>
-__global__ void k_filter_build(const int* __restrict__ DL, uint32_t width, uint32_t gshift, int32_t ybase,
-                               uint32_t ys, W* __restrict__ F, uint32_t ngroups) {
-    const uint32_t gi = blockIdx.x * blockDim.x + threadIdx.x;
-    if (gi >= ngroups) return;
+__device__ __forceinline__ uint32_t lds_w(uint32_t addr) {
+    if (sizeof(W) == 2) {
+        uint16_t v;
+        asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
+        return v;
+    } else {
+        return lds_u32(addr);
+    }
+}
+
+// One warp per group: the lanes stride over the group's columns (coalesced
+// 8-byte loads), then shuffle-reduce max lo / min hi / any-empty.  Word
+// `ngroups` (the sink) and a partial last group are "never".
+template <typename W>
+__global__ void __launch_bounds__(256) k_filter_build(const int* __restrict__ DL, uint32_t width, uint32_t gshift,
+                                                      uint32_t ys, W* __restrict__ F, uint32_t ngroups) {
+    const uint32_t gi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    if (gi > ngroups) return;
     const int2* gL = reinterpret_cast<const int2*>(DL);
     const uint32_t c0 = gi << gshift;
-    const uint32_t c1 = min(width, c0 + (1u << gshift));
-    long long maxlo = LLONG_MIN, minhi = LLONG_MAX;
+    const uint32_t c1 = c0 + (1u << gshift);
+    const bool full = gi < ngroups && c1 <= width;
+    int maxlo = INT32_MIN, minhi = INT32_MAX;
     bool empty = false;
-    for (uint32_t c = c0; c < c1; ++c) {
-        const int2 e = ld_cg2(gL + c);
-        const long long lo = e.x, hi = ~e.y;
-        if (lo > hi) {
-            empty = true;
-            break;
+    if (full)
+        for (uint32_t c = c0 + lane; c < c1; c += 32) {
+            const int2 e = ld_cg2(gL + c);
+            const int lo = e.x, hi = ~e.y;
+            empty |= lo > hi;
+            maxlo = max(maxlo, lo);
+            minhi = min(minhi, hi);
         }
-        maxlo = lo > maxlo ? lo : maxlo;
-        minhi = hi < minhi ? hi : minhi;
+    empty = __any_sync(0xffffffffu, empty);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        maxlo = max(maxlo, __shfl_xor_sync(0xffffffffu, maxlo, o));
+        minhi = min(minhi, __shfl_xor_sync(0xffffffffu, minhi, o));
     }
-    constexpr long long M = FW<W>::kMask;
+    if (lane) return;
     W word = FW<W>::kNever;
-    if (!empty && c0 < c1) {
+    if (full && !empty) {
+        constexpr long long M = FW<W>::kMask;
         const long long q = 1ll << ys;
-        long long a = maxlo - ybase;
-        long long fa = a <= 0 ? 0 : (a + q - 1) / q;
-        long long fb = (minhi - ybase + 1) >= 0 ? (minhi - ybase + 1) / q - 1 : -1;
+        const long long a = (long long)maxlo - 1;
+        const long long fa = a <= 0 ? 0 : (a + q - 1) / q;
+        long long fb = minhi >= 0 ? (long long)minhi / q - 1 : -1;
         if (fb > M) fb = M;
-        if (fa <= fb && fa <= M && fb >= 0) word = (W)((uint32_t)fa | ((uint32_t)fb << FW<W>::kHalf));
+        if (fa <= fb) {
+            const long long span = (fb - fa + 1) < M ? (fb - fa + 1) : M;
+            word = (W)((uint32_t)fa | ((uint32_t)span << FW<W>::kHalf));
+        }
     }
     F[gi] = word;
 }
 
 // F == nullptr starts from an all-"never skip" table (the warm-up pass:
-// every point is settled in L2, RED-only, building the first snapshot).
-template <typename W, bool VALIDATE, bool READ_FIRST, bool TMA>
+// every point is settled in L2, building the first snapshot).  Validated
+// input only (y in [1, q]); the host guarantees wcheck == width.
+template <typename W, bool READ_FIRST, bool TMA>
 __global__ void __launch_bounds__(kThreads) k_reduce_filter(const int32_t* __restrict__ xy, uint64_t n,
-                                                            Geo g, uint32_t width, uint32_t gshift,
-                                                            int32_t ybase, uint32_t ys,
+                                                            Geo g, uint32_t width, uint32_t gshift, uint32_t ys,
                                                             const W* __restrict__ F, uint32_t ngroups, int stages,
                                                             int* __restrict__ DL) {
     extern __shared__ uint4 sF4[];
     W* sF = reinterpret_cast<W*>(sF4);
-    uint8_t* ring = reinterpret_cast<uint8_t*>(sF4) + table_span((size_t)ngroups * sizeof(W));
+    const uint32_t nwords = ngroups + 1;
+    uint8_t* ring = reinterpret_cast<uint8_t*>(sF4) + table_span((size_t)nwords * sizeof(W));
     {
         const uint32_t per4 = 16 / sizeof(W);
-        const uint32_t n4 = ngroups / per4;
+        const uint32_t n4 = nwords / per4;
         if (F) {
             const uint4* F4 = reinterpret_cast<const uint4*>(F);
             for (uint32_t i = threadIdx.x; i < n4; i += blockDim.x) sF4[i] = __ldcg(F4 + i);
-            for (uint32_t i = n4 * per4 + threadIdx.x; i < ngroups; i += blockDim.x) sF[i] = F[i];
+            for (uint32_t i = n4 * per4 + threadIdx.x; i < nwords; i += blockDim.x) sF[i] = F[i];
         } else {
-            for (uint32_t i = threadIdx.x; i < ngroups; i += blockDim.x) sF[i] = FW<W>::kNever;
+            for (uint32_t i = threadIdx.x; i < nwords; i += blockDim.x) sF[i] = FW<W>::kNever;
         }
     }
     __syncthreads();
     constexpr uint32_t H = FW<W>::kHalf, HM = FW<W>::kMask;
-    const uint32_t ulim = HM << ys | ((1u << ys) - 1u);
-    // (uint32) y - ybase wraps for y < ybase; then it exceeds ulim and misses.
-    auto hit = [&](uint32_t s, int32_t y) {
-        const uint32_t w = sF[s >> gshift];
-        const uint32_t d = (uint32_t)y - (uint32_t)ybase;
-        const uint32_t u = d >> ys;
-        return d <= ulim && u >= (w & HM) && u <= (w >> H);
+    const uint32_t tbase = (uint32_t)__cvta_generic_to_shared(sF4);
+    uint32_t bad = 0;
+    // Branch-free hit test: true when the point must be settled.  An invalid
+    // x reads a never-skip word; an invalid y has u > fb (or wraps), so it
+    // misses as well and is caught in the miss path.
+    auto test = [&](int32_t x, int32_t y, uint32_t& s, uint32_t& w) -> bool {
+        s = min(slot_of(x, g.base), width);
+        w = lds_w<W>(tbase + (s >> gshift) * (uint32_t)sizeof(W));
+        return (((uint32_t)y - 1u) >> ys) - (w & HM) >= (w >> H);
     };
-    bool bad = false;
-    auto one = [&](int32_t x, int32_t y) {
-        uint32_t s[1];
-        int yy[1] = {y};
-        if (!accept<VALIDATE>(g, x, y, s[0])) {
-            bad = true;
-            return;
-        }
-        settle_misses<true>(hit(s[0], y) ? 0u : 1u, s, yy, DL);
+    auto valid = [&](uint32_t s, int32_t y) {
+        const bool ok = (s < g.wcheck) & ((uint32_t)y - 1u < g.qmax);
+        bad |= !ok;
+        return ok;
     };
     // RED-only misses are one-sided where the word allows: u <= fb means
     // y <= min_hi of the group, so only lo can move; u >= fa means
     // y >= max_lo, so only hi can move.
-    auto one_red = [&](int32_t x, int32_t y) {
-        uint32_t s;
-        if (!accept<VALIDATE>(g, x, y, s)) {
-            bad = true;
-            return;
+    auto settle_red = [&](uint32_t s, int32_t y, uint32_t w) {
+        if (!valid(s, y)) return;
+        const uint32_t u = ((uint32_t)y - 1u) >> ys;
+        const uint32_t fa = w & HM, span = w >> H;
+        if (span == 0 || u > fa) red_min(DL + 2ull * s + 1, ~y);  // not known below min_hi
+        if (span == 0 || u < fa) red_min(DL + 2ull * s, y);       // not known above max_lo
+    };
+    auto one = [&](int32_t x, int32_t y) {
+        uint32_t s, w;
+        if (!test(x, y, s, w)) return;
+        if (READ_FIRST) {
+            if (!valid(s, y)) return;
+            uint32_t ss[1] = {s};
+            int yy[1] = {y};
+            settle_misses<true>(1u, ss, yy, DL);
+        } else {
+            settle_red(s, y, w);
         }
-        const uint32_t w = sF[s >> gshift];
-        const uint32_t d = (uint32_t)y - (uint32_t)ybase;
-        const uint32_t u = d >> ys;
-        const uint32_t fa = w & HM, fb = w >> H;
-        // Only a usable word (fa <= fb) bounds the group; the empty word
-        // (fa = all ones, fb = 0) says nothing about either side.
-        const bool in = d <= ulim && fa <= fb;
-        const bool above_lo = in && u >= fa;  // y >= max_lo of the group
-        const bool below_hi = in && u <= fb;  // y <= min_hi of the group
-        if (above_lo && below_hi) return;
-        if (!above_lo) red_min(DL + 2ull * s, y);
-        if (!below_hi) red_min(DL + 2ull * s + 1, ~y);
     };
     if (READ_FIRST) {
+        // Four tests, then the misses' L2 reads all in flight together.
         stream_points<TMA>(
             xy, n, ring, stages,
             [&](const int4& a, const int4& b) {
-                int x[4], y[4];
-                uint32_t s[4], miss = 0;
-                unpack4(a, b, x, y);
+                const int y[4] = {a.y, a.w, b.y, b.w};
+                uint32_t s[4], w[4], miss = 0;
+                miss |= (uint32_t)test(a.x, a.y, s[0], w[0]);
+                miss |= (uint32_t)test(a.z, a.w, s[1], w[1]) << 1;
+                miss |= (uint32_t)test(b.x, b.y, s[2], w[2]) << 2;
+                miss |= (uint32_t)test(b.z, b.w, s[3], w[3]) << 3;
+                if (miss) {
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    if (!accept<VALIDATE>(g, x[k], y[k], s[k]))
-                        bad = true;
-                    else if (!hit(s[k], y[k]))
-                        miss |= 1u << k;
+                    for (int k = 0; k < 4; ++k)
+                        if (((miss >> k) & 1) && !valid(s[k], y[k])) miss &= ~(1u << k);
+                    settle_misses<true>(miss, s, y, DL);
                 }
-                settle_misses<true>(miss, s, y, DL);
             },
             one);
     } else {
-        stream_points<TMA>(xy, n, ring, stages, per_point4(one_red), one_red);
+        stream_points<TMA>(xy, n, ring, stages, per_point4(one), one);
     }
-    flag_error(bad, DL, width);
+    flag_error(bad != 0, DL, width);
 }
 
 // ------------------------------------------------------------ sampled
@@ -1046,49 +1073,51 @@ int blocks_for(chp_ctx* ctx, const void* fn, size_t smem, int cap_per_sm) {
         CHP_LAUNCHED(ctx);                                                                               \
     } while (0)
 
-// Column-group snapshot filter in phases: a warm-up pass (n/64) through the
-// same kernel with an empty table (every point settled in L2, RED-only),
-// then snapshot -> n/8 -> snapshot -> the rest.  The table (W = 16-bit
+// Column-group snapshot filter in phases of doubling length (below), each
+// against a fresh snapshot of DL.  The table (W = 16-bit
 // words with 8-bit halves, or 32-bit words with 16-bit halves) is sized to
 // `fbudget` bytes; the rest of shared memory holds the TMA ring.
-template <typename W, bool V>
+template <typename W>
 int run_group_filter(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, const Geo& g, uint32_t w, int64_t q,
                      uint32_t flags, size_t fbudget, int32_t* d_L) {
     uint32_t ys = 0;
     while ((uint64_t)(q - 1) >> ys > FW<W>::kMask) ++ys;
     uint32_t gshift = 0;
-    while (((uint64_t)(w + (1u << gshift) - 1) >> gshift) * sizeof(W) > fbudget) ++gshift;
+    while ((((uint64_t)(w + (1u << gshift) - 1) >> gshift) + 1) * sizeof(W) > fbudget) ++gshift;
     const uint32_t ngroups = (w + (1u << gshift) - 1) >> gshift;
-    int rc = chp_ensure(ctx, ctx->filter, (size_t)ngroups * sizeof(W) + 16);
+    int rc = chp_ensure(ctx, ctx->filter, (size_t)(ngroups + 1) * sizeof(W) + 16);
     if (rc) return rc;
-    const Plan pl = plan_for(ctx, (size_t)ngroups * sizeof(W), flags, false);
-    // Small groups: a miss is usually a real update -> RED directly.
-    // Wide groups: many misses are not -> read the slot first.
-    bool read_first = gshift >= 3;
-    if (flags & CHP_REDUCE_MISS_RED) read_first = false;
-    if (flags & CHP_REDUCE_MISS_READ) read_first = true;
-    const uint64_t warm = std::min<uint64_t>(n, n / 64) & ~1ull;
-    if (warm)
-        CHP_LAUNCH_PLANNED(ctx, pl, (k_reduce_filter<W, V, false, true>), (k_reduce_filter<W, V, false, false>), d_xy,
-                           warm, g, w, gshift, 1, ys, (const W*)nullptr, ngroups, pl.stages, d_L);
-    uint64_t done = warm;
-    const uint64_t bounds[2] = {std::min<uint64_t>(n, warm + n / 8) & ~1ull, n};
-    for (int ph = 0; ph < 2 && done < n; ++ph) {
-        k_filter_build<W><<<(ngroups + 255) / 256, 256, 0, ctx->stream>>>(d_L, w, gshift, 1, ys, (W*)ctx->filter.p,
-                                                                         ngroups);
+    const Plan pl = plan_for(ctx, (size_t)(ngroups + 1) * sizeof(W), flags, false);
+    // Misses RED (one-sided where the word allows) without reading the slot:
+    // with the doubling schedule the misses are few, and a warp that waits
+    // on an L2 read per miss group stalls the stream (C4: 471 vs 388 Gpts/s).
+    const bool read_first = (flags & CHP_REDUCE_MISS_READ) != 0;
+    auto pass = [&](const int32_t* xy, uint64_t cnt, const W* F) {
+        if (read_first)
+            CHP_LAUNCH_PLANNED(ctx, pl, (k_reduce_filter<W, true, true>), (k_reduce_filter<W, true, false>), xy, cnt,
+                               g, w, gshift, ys, F, ngroups, pl.stages, d_L);
+        else
+            CHP_LAUNCH_PLANNED(ctx, pl, (k_reduce_filter<W, false, true>), (k_reduce_filter<W, false, false>), xy,
+                               cnt, g, w, gshift, ys, F, ngroups, pl.stages, d_L);
+        return CHP_OK;
+    };
+    // Phases double in length: warm-up n/2^kw (default n/256) with an empty
+    // table, then [d, 2d) against a snapshot of DL taken at d.  The snapshot
+    // at d leaves ~1/d of the later points outside the band (SURVEY-style
+    // simulation of C4: group hit rate 53% at n/64, 94% at n/7, 98% at n/2),
+    // so doubling keeps the misses of every phase about equal.
+    const uint32_t kfield = (flags >> 16) & 7;
+    const uint32_t kw = kfield ? kfield + 3 : 8;  // C4: kw 8 471, 9 464, 10 462 Gpts/s
+    // (Inputs under 4 Mi points: one pass with the empty table.)
+    const uint64_t warm = n < (1ull << 22) ? n : (n >> kw) & ~1ull;
+    if ((rc = pass(d_xy, warm, nullptr))) return rc;
+    for (uint64_t done = warm; done < n;) {
+        k_filter_build<W><<<(ngroups + 1 + 7) / 8, 256, 0, ctx->stream>>>(d_L, w, gshift, ys, (W*)ctx->filter.p,
+                                                                        ngroups);
         CHP_LAUNCHED(ctx);
-        const uint64_t end = bounds[ph];
-        if (end > done) {
-            if (read_first)
-                CHP_LAUNCH_PLANNED(ctx, pl, (k_reduce_filter<W, V, true, true>), (k_reduce_filter<W, V, true, false>),
-                                   d_xy + 2 * done, end - done, g, w, gshift, 1, ys, (const W*)ctx->filter.p,
-                                   ngroups, pl.stages, d_L);
-            else
-                CHP_LAUNCH_PLANNED(ctx, pl, (k_reduce_filter<W, V, false, true>),
-                                   (k_reduce_filter<W, V, false, false>), d_xy + 2 * done, end - done, g, w, gshift,
-                                   1, ys, (const W*)ctx->filter.p, ngroups, pl.stages, d_L);
-            done = end;
-        }
+        const uint64_t stop = std::min<uint64_t>(n, 2 * done);
+        if ((rc = pass(d_xy + 2 * done, stop - done, (const W*)ctx->filter.p))) return rc;
+        done = stop;
     }
     return CHP_OK;
 }
@@ -1140,6 +1169,7 @@ extern "C" int chp_reduce(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t
 
     const uint32_t wpad8 = (w + 8) & ~7u;  // >= w + 1: slot w is the invalid-x sink
     const bool fits_sampled = yknown && g.wcheck == w && (size_t)wpad8 * 2 <= budget;
+    const bool fits_filter = yknown && g.wcheck == w;  // invalid x must clamp onto the sink
 
     enum { V_GLOBAL, V_SMEM32, V_SMEM16, V_FILTER8, V_FILTER, V_SAMPLED } v;
     if (flags & CHP_REDUCE_FORCE_GLOBAL) v = V_GLOBAL;
@@ -1147,11 +1177,11 @@ extern "C" int chp_reduce(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t
     else if ((flags & CHP_REDUCE_FORCE_SMEM32) && fits32) v = V_SMEM32;
     else if ((flags & CHP_REDUCE_FORCE_SMEM16) && fits16) v = V_SMEM16;
     else if ((flags & CHP_REDUCE_FORCE_FILTER8) && fits_f8) v = V_FILTER8;
-    else if ((flags & CHP_REDUCE_FORCE_FILTER) && yknown) v = V_FILTER;
+    else if ((flags & CHP_REDUCE_FORCE_FILTER) && fits_filter) v = V_FILTER;
     else if (fits16) v = V_SMEM16;  // measured: 1.05-1.24x smem32 (C3, C5)
     else if (fits32) v = V_SMEM32;
     else if (fits_sampled) v = V_SAMPLED;
-    else if (yknown) v = V_FILTER;
+    else if (fits_filter) v = V_FILTER;
     else v = V_GLOBAL;
 
     // The sampled variant initialises DL inside its sample pass.
@@ -1276,11 +1306,9 @@ extern "C" int chp_reduce(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t
             const size_t fbudget = (flags & CHP_REDUCE_FILTER_SMALL) ? 100 * 1024 : budget;
             int rc;
             if (flags & CHP_REDUCE_FILTER16)
-                rc = validate ? run_group_filter<uint32_t, true>(ctx, d_xy, n, g, w, q, flags, fbudget, d_L)
-                              : run_group_filter<uint32_t, false>(ctx, d_xy, n, g, w, q, flags, fbudget, d_L);
+                rc = run_group_filter<uint32_t>(ctx, d_xy, n, g, w, q, flags, fbudget, d_L);
             else
-                rc = validate ? run_group_filter<uint16_t, true>(ctx, d_xy, n, g, w, q, flags, fbudget, d_L)
-                              : run_group_filter<uint16_t, false>(ctx, d_xy, n, g, w, q, flags, fbudget, d_L);
+                rc = run_group_filter<uint16_t>(ctx, d_xy, n, g, w, q, flags, fbudget, d_L);
             if (rc) return rc;
             ctx->variant = (flags & CHP_REDUCE_FILTER16) ? "filter16" : "filter";
             return CHP_OK;

@@ -28,6 +28,11 @@ VARIANTS = {
     "sampled": _lib.REDUCE_FORCE_SAMPLED,
     "sampled_fused": _lib.REDUCE_FORCE_SAMPLED | 16384,
     "smem16_tma": _lib.REDUCE_FORCE_SMEM16 | 4096,
+    # group filter: 32-bit words, RED-only and read-first misses, TMA ring
+    "filter16": _lib.REDUCE_FORCE_FILTER | 512,
+    "filter_red": _lib.REDUCE_FORCE_FILTER | 128,
+    "filter_read_tma": _lib.REDUCE_FORCE_FILTER | 256 | 4096,
+    "sampled_tma": _lib.REDUCE_FORCE_SAMPLED | 4096,
 }
 
 
