@@ -446,47 +446,60 @@ __device__ __forceinline__ uint32_t lds_w(uint32_t addr) {
     }
 }
 
-// One warp per group: the lanes stride over the group's columns (coalesced
-// 8-byte loads), then shuffle-reduce max lo / min hi / any-empty.  Word
+// One thread per group, its columns read as 16-byte pairs with up to 8
+// loads in flight (a warp-per-group form left half the lanes idle and ran
+// one round trip per wave: 16 us per snapshot at p = 2^20).  Word
 // `ngroups` (the sink) and a partial last group are "never".
 template <typename W>
 __global__ void __launch_bounds__(256) k_filter_build(const int* __restrict__ DL, uint32_t width, uint32_t gshift,
                                                       uint32_t ys, W* __restrict__ F, uint32_t ngroups) {
-    const uint32_t gi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t gi = blockIdx.x * blockDim.x + threadIdx.x;
     if (gi > ngroups) return;
-    const int2* gL = reinterpret_cast<const int2*>(DL);
     const uint32_t c0 = gi << gshift;
     const uint32_t c1 = c0 + (1u << gshift);
-    const bool full = gi < ngroups && c1 <= width;
-    int maxlo = INT32_MIN, minhi = INT32_MAX;
-    bool empty = false;
-    if (full)
-        for (uint32_t c = c0 + lane; c < c1; c += 32) {
-            const int2 e = ld_cg2(gL + c);
-            const int lo = e.x, hi = ~e.y;
+    W word = FW<W>::kNever;
+    if (gi < ngroups && c1 <= width) {
+        int maxlo = INT32_MIN, minhi = INT32_MAX;
+        bool empty = false;
+        auto fold = [&](int lo, int nhi) {
+            const int hi = ~nhi;
             empty |= lo > hi;
             maxlo = max(maxlo, lo);
             minhi = min(minhi, hi);
-        }
-    empty = __any_sync(0xffffffffu, empty);
+        };
+        if (gshift >= 1 && !(reinterpret_cast<uintptr_t>(DL) & 15)) {  // 16-byte aligned pairs
+            const int4* p4 = reinterpret_cast<const int4*>(DL) + (c0 >> 1);
+            const uint32_t n4 = 1u << (gshift - 1);
+            for (uint32_t i = 0; i < n4; i += 8) {
+                int4 q[8];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        maxlo = max(maxlo, __shfl_xor_sync(0xffffffffu, maxlo, o));
-        minhi = min(minhi, __shfl_xor_sync(0xffffffffu, minhi, o));
-    }
-    if (lane) return;
-    W word = FW<W>::kNever;
-    if (full && !empty) {
-        constexpr long long M = FW<W>::kMask;
-        const long long q = 1ll << ys;
-        const long long a = (long long)maxlo - 1;
-        const long long fa = a <= 0 ? 0 : (a + q - 1) / q;
-        long long fb = minhi >= 0 ? (long long)minhi / q - 1 : -1;
-        if (fb > M) fb = M;
-        if (fa <= fb) {
-            const long long span = (fb - fa + 1) < M ? (fb - fa + 1) : M;
-            word = (W)((uint32_t)fa | ((uint32_t)span << FW<W>::kHalf));
+                for (int k = 0; k < 8; ++k)
+                    if (i + k < n4) q[k] = __ldcg(p4 + i + k);
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    if (i + k < n4) {
+                        fold(q[k].x, q[k].y);
+                        fold(q[k].z, q[k].w);
+                    }
+            }
+        } else {
+            const int2* p2 = reinterpret_cast<const int2*>(DL);
+            for (uint32_t c = c0; c < c1; ++c) {
+                const int2 e = ld_cg2(p2 + c);
+                fold(e.x, e.y);
+            }
+        }
+        if (!empty) {
+            constexpr long long M = FW<W>::kMask;
+            const long long q = 1ll << ys;
+            const long long a = (long long)maxlo - 1;
+            const long long fa = a <= 0 ? 0 : (a + q - 1) / q;
+            long long fb = minhi >= 0 ? (long long)minhi / q - 1 : -1;
+            if (fb > M) fb = M;
+            if (fa <= fb) {
+                const long long span = (fb - fa + 1) < M ? (fb - fa + 1) : M;
+                word = (W)((uint32_t)fa | ((uint32_t)span << FW<W>::kHalf));
+            }
         }
     }
     F[gi] = word;
@@ -1112,8 +1125,8 @@ int run_group_filter(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, const Geo& g
     const uint64_t warm = n < (1ull << 22) ? n : (n >> kw) & ~1ull;
     if ((rc = pass(d_xy, warm, nullptr))) return rc;
     for (uint64_t done = warm; done < n;) {
-        k_filter_build<W><<<(ngroups + 1 + 7) / 8, 256, 0, ctx->stream>>>(d_L, w, gshift, ys, (W*)ctx->filter.p,
-                                                                        ngroups);
+        k_filter_build<W><<<(ngroups + 1 + 255) / 256, 256, 0, ctx->stream>>>(d_L, w, gshift, ys,
+                                                                            (W*)ctx->filter.p, ngroups);
         CHP_LAUNCHED(ctx);
         const uint64_t stop = std::min<uint64_t>(n, 2 * done);
         if ((rc = pass(d_xy + 2 * done, stop - done, (const W*)ctx->filter.p))) return rc;
