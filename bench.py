@@ -340,9 +340,12 @@ def main():
             t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_ms = float(t.item())
-        e2e = {"value": total_points / (e2e_ms * 1e-3) / 1e9, "unit": "Gpoints/s", "h2d_bytes_per_step": n * 8,
+        h2d = ctx.last_h2d_bytes
+        e2e = {"value": total_points / (e2e_ms * 1e-3) / 1e9, "unit": "Gpoints/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": int(s_out[0]) * 8 + 64, "ms_per_step": e2e_ms,
-               "path": "chp_pipeline_host (pinned input, 128 MiB chunks, H2D overlapped with K1)"}
+               "path": "chp_pipeline_host (pinned int32 input; 16 Mi-point chunks, "
+                       + ("packed to 16-bit slot|y words on host threads, " if h2d < n * 8 else "")
+                       + "H2D overlapped with K1)"}
         del host
 
     base = None

@@ -62,6 +62,9 @@ uint64_t chp_launch_count(const chp_ctx* ctx);
 /* Kernel-variant name chosen by the last chp_reduce ("smem32", "smem16",
  * "global", "filter"). */
 const char* chp_last_variant(const chp_ctx* ctx);
+/* Host->device bytes the last host pipeline call (chp_*_host) copied: 8 per
+ * point as int32 pairs, 4 per point when the input was packed to 16 bits. */
+uint64_t chp_last_h2d_bytes(const chp_ctx* ctx);
 
 /* ------------------------------------------------- device-form L ("DL")
  * int32[chp_dl_len(width)] = width pairs (lo, ~hi), empty = (INT32_MAX,
@@ -89,6 +92,7 @@ uint64_t chp_dl_len(int64_t width);
 #define CHP_REDUCE_SAMPLE_K(k) ((uint32_t)(k) << 16) /* tuning: sample n/2^k (k in 1..7, default 3) */
 /* bits 19-21: group-filter phase-A fraction n/2^ka (default 3) */
 #define CHP_REDUCE_SAMPLE_TMA (1u << 22) /* tuning: sample pass streams through the TMA ring */
+#define CHP_PIPELINE_NO_PACK (1u << 23) /* host pipelines: always send int32 pairs (no 16-bit packing) */
 
 /* Algorithm 1 over n int32 (x,y) pairs at d_xy (8-byte aligned).  Slot of a
  * point is x - x_off - 1; a point is valid when that slot is in [0,width)

@@ -48,6 +48,7 @@ def load() -> ctypes.CDLL:
         "chp_ctx_sync": (c_int, [vp]),
         "chp_launch_count": (c_uint64, [vp]),
         "chp_last_variant": (c_char_p, [vp]),
+        "chp_last_h2d_bytes": (c_uint64, [vp]),
         "chp_dl_len": (c_uint64, [c_int64]),
         "chp_reduce": (c_int, [vp, vp, c_uint64, c_int64, c_int64, c_int64, vp, c_uint32]),
         "chp_dl_init": (c_int, [vp, vp, c_int64]),
@@ -76,7 +77,7 @@ def load() -> ctypes.CDLL:
 # Every symbol include/chp_b200.h declares (checked by tests without a GPU).
 ABI_SYMBOLS = (
     "chp_ctx_create", "chp_ctx_destroy", "chp_last_error", "chp_ctx_set_stream", "chp_ctx_use_own_stream", "chp_ctx_stream",
-    "chp_ctx_sync", "chp_launch_count", "chp_last_variant", "chp_dl_len", "chp_reduce", "chp_dl_init",
+    "chp_ctx_sync", "chp_launch_count", "chp_last_variant", "chp_last_h2d_bytes", "chp_dl_len", "chp_reduce", "chp_dl_init",
     "chp_check", "chp_dl_from_pairs", "chp_polyline_host", "chp_compact", "chp_ns_chain", "chp_hull", "chp_bounds", "chp_translate", "chp_translate_host",
     "chp_pipeline_host", "chp_precondition_host", "chp_generate", "chp_generate_host",
 )

@@ -6,11 +6,85 @@
 // previous chunk on the compute stream (two device buffers, event-ordered),
 // then K3 (+K4) run on device and only L / the chain / the hull come back.
 #include <algorithm>
+#include <condition_variable>
+#include <cstdlib>
 #include <cstring>
+#include <functional>
+#include <immintrin.h>
+#include <mutex>
+#include <thread>
+#include <vector>
 
 #include "chp_internal.cuh"
 
 namespace {
+
+// Persistent host workers for the packed pipeline: run(f) calls f(i) for
+// i in [0, parts) on the workers and the caller, and returns when all are
+// done.  One job at a time (the pipeline is single-threaded per context).
+class HostPool {
+  public:
+    explicit HostPool(int workers) {
+        for (int i = 0; i < workers; ++i) th_.emplace_back([this, i] { loop(i + 1); });
+    }
+    ~HostPool() {
+        {
+            std::lock_guard<std::mutex> g(m_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : th_) t.join();
+    }
+    int parts() const { return (int)th_.size() + 1; }
+    void run(const std::function<void(int)>& f) {
+        {
+            std::lock_guard<std::mutex> g(m_);
+            job_ = &f;
+            pending_ = (int)th_.size();
+            ++gen_;
+        }
+        cv_.notify_all();
+        f(0);
+        std::unique_lock<std::mutex> lk(m_);
+        done_.wait(lk, [this] { return pending_ == 0; });
+        job_ = nullptr;
+    }
+
+  private:
+    void loop(int id) {
+        uint64_t seen = 0;
+        for (;;) {
+            const std::function<void(int)>* job;
+            {
+                std::unique_lock<std::mutex> lk(m_);
+                cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+                if (stop_) return;
+                seen = gen_;
+                job = job_;
+            }
+            (*job)(id);
+            {
+                std::lock_guard<std::mutex> g(m_);
+                if (--pending_ == 0) done_.notify_one();
+            }
+        }
+    }
+    std::vector<std::thread> th_;
+    std::mutex m_;
+    std::condition_variable cv_, done_;
+    const std::function<void(int)>* job_ = nullptr;
+    uint64_t gen_ = 0;
+    int pending_ = 0;
+    bool stop_ = false;
+};
+
+HostPool* pool_of(chp_ctx* ctx) {
+    if (!ctx->pool) {
+        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        ctx->pool = new HostPool((int)std::min(hw, 32u) - 1);
+    }
+    return static_cast<HostPool*>(ctx->pool);
+}
 
 constexpr uint64_t kChunkPts = 16ull << 20;  // 16 Mi points = 128 MiB per chunk
 
@@ -67,6 +141,7 @@ int stream_chunks(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, Launch&& launch
         CHP_CUDA(ctx, cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_consumed[b], 0));
         CHP_CUDA(ctx, cudaMemcpyAsync(ctx->stage_dev[b].p, src, (size_t)m * 8, cudaMemcpyHostToDevice,
                                       ctx->copy_stream));
+        ctx->h2d_bytes += (uint64_t)m * 8;
         CHP_CUDA(ctx, cudaEventRecord(ctx->ev_copied[b], ctx->copy_stream));
         CHP_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_copied[b], 0));
         if ((rc = launch((const int32_t*)ctx->stage_dev[b].p, m))) return rc;
@@ -75,12 +150,130 @@ int stream_chunks(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, Launch&& launch
     return CHP_OK;
 }
 
+// Host side of the packed pipeline: (x, y) -> slot | (y - 1) << 16 for a
+// slice, returning nonzero if any point is invalid (slot >= wcheck or y
+// outside [1, q]).  SSE2, 4 points per step, non-temporal stores: the pinned
+// staging is only read by the DMA engine, so skipping the read-for-ownership
+// saves a third of the host memory traffic.
+uint32_t pack16(const int32_t* __restrict__ src, uint32_t* __restrict__ dst, uint64_t m, uint32_t base,
+                uint32_t wcheck, uint32_t qmax) {
+    uint32_t bad = 0;
+    uint64_t i = 0;
+    auto one = [&](uint64_t k) {
+        const uint32_t s = (uint32_t)src[2 * k] - base;
+        const uint32_t ym1 = (uint32_t)src[2 * k + 1] - 1u;
+        bad |= (uint32_t)(s >= wcheck) | (uint32_t)(ym1 >= qmax);
+        dst[k] = s | (ym1 << 16);
+    };
+    for (; i < m && (reinterpret_cast<uintptr_t>(dst + i) & 15); ++i) one(i);
+    const __m128i vbase = _mm_set1_epi32((int)base), vone = _mm_set1_epi32(1);
+    const __m128i sign = _mm_set1_epi32((int)0x80000000u);
+    const __m128i wlim = _mm_set1_epi32((int)(wcheck ^ 0x80000000u)), qlim = _mm_set1_epi32((int)(qmax ^ 0x80000000u));
+    __m128i okv = _mm_set1_epi32(-1);
+    for (; i + 4 <= m; i += 4) {
+        const __m128i a = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + 2 * i));      // x0 y0 x1 y1
+        const __m128i b = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + 2 * i + 4));  // x2 y2 x3 y3
+        const __m128i a2 = _mm_shuffle_epi32(a, _MM_SHUFFLE(3, 1, 2, 0));                     // x0 x1 y0 y1
+        const __m128i b2 = _mm_shuffle_epi32(b, _MM_SHUFFLE(3, 1, 2, 0));                     // x2 x3 y2 y3
+        const __m128i s = _mm_sub_epi32(_mm_unpacklo_epi64(a2, b2), vbase);
+        const __m128i ym1 = _mm_sub_epi32(_mm_unpackhi_epi64(a2, b2), vone);
+        // unsigned v < lim  <=>  signed (v ^ 2^31) < (lim ^ 2^31)
+        okv = _mm_and_si128(okv, _mm_cmplt_epi32(_mm_xor_si128(s, sign), wlim));
+        okv = _mm_and_si128(okv, _mm_cmplt_epi32(_mm_xor_si128(ym1, sign), qlim));
+        _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i), _mm_or_si128(s, _mm_slli_epi32(ym1, 16)));
+    }
+    for (; i < m; ++i) one(i);
+    _mm_sfence();  // the stores are weakly ordered; the DMA is enqueued after this returns
+    return bad | (uint32_t)(_mm_movemask_epi8(okv) != 0xFFFF);
+}
+
+// Packed form of stream_chunks for width <= 2^16 and 1 <= y <= q <= 2^16:
+// host workers pack chunk k into pinned 4-byte/point staging while the DMA
+// of chunk k-1 is in flight, so PCIe carries half the bytes; on the device
+// k_unpack16 restores int32 pairs and launch() consumes them.  *bad is set
+// when any point is invalid (the caller fails the call).
+template <typename Launch>
+int stream_chunks_packed(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t x_off, uint32_t wcheck,
+                         uint32_t qmax, bool* bad, Launch&& launch) {
+    *bad = false;
+    if (n == 0) return CHP_OK;
+    const uint64_t chunk = std::min<uint64_t>(kChunkPts, n);
+    int rc;
+    for (int b = 0; b < 2; ++b) {
+        if ((rc = chp_ensure(ctx, ctx->stage_dev[b], (size_t)chunk * 4))) return rc;
+        if ((rc = chp_ensure(ctx, ctx->unpack_dev[b], (size_t)chunk * 8))) return rc;
+    }
+    if (ctx->pack_bytes < (size_t)chunk * 4) {
+        for (int b = 0; b < 2; ++b) {
+            if (ctx->pack_host[b]) cudaFreeHost(ctx->pack_host[b]);
+            ctx->pack_host[b] = nullptr;
+        }
+        for (int b = 0; b < 2; ++b) CHP_CUDA(ctx, cudaMallocHost(&ctx->pack_host[b], (size_t)chunk * 4));
+        ctx->pack_bytes = (size_t)chunk * 4;
+    }
+    HostPool* pool = pool_of(ctx);
+    const uint32_t base = (uint32_t)(int32_t)(x_off + 1);
+    for (int b = 0; b < 2; ++b) {
+        CHP_CUDA(ctx, cudaEventRecord(ctx->ev_consumed[b], ctx->stream));
+        CHP_CUDA(ctx, cudaEventRecord(ctx->ev_copied[b], ctx->copy_stream));
+    }
+    uint32_t any_bad = 0;
+    std::vector<uint32_t> part_bad((size_t)pool->parts());
+    uint64_t k = 0;
+    for (uint64_t off = 0; off < n; off += chunk, ++k) {
+        const int b = (int)(k & 1);
+        const uint64_t m = std::min<uint64_t>(chunk, n - off);
+        // The DMA out of this staging buffer (chunk k-2) must have finished.
+        CHP_CUDA(ctx, cudaEventSynchronize(ctx->ev_copied[b]));
+        uint32_t* dst = static_cast<uint32_t*>(ctx->pack_host[b]);
+        const int32_t* src = h_xy + 2 * off;
+        const int parts = pool->parts();
+        pool->run([&](int i) {
+            const uint64_t lo = (m * (uint64_t)i / parts) & ~3ull;
+            const uint64_t hi = i + 1 == parts ? m : (m * (uint64_t)(i + 1) / parts) & ~3ull;
+            part_bad[(size_t)i] = pack16(src + 2 * lo, dst + lo, hi - lo, base, wcheck, qmax);
+        });
+        for (uint32_t v : part_bad) any_bad |= v;
+        CHP_CUDA(ctx, cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_consumed[b], 0));
+        CHP_CUDA(ctx, cudaMemcpyAsync(ctx->stage_dev[b].p, dst, (size_t)m * 4, cudaMemcpyHostToDevice,
+                                      ctx->copy_stream));
+        ctx->h2d_bytes += (uint64_t)m * 4;
+        CHP_CUDA(ctx, cudaEventRecord(ctx->ev_copied[b], ctx->copy_stream));
+        CHP_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_copied[b], 0));
+        if ((rc = chp_unpack16(ctx, (const uint32_t*)ctx->stage_dev[b].p, m, (int32_t)base,
+                               (int32_t*)ctx->unpack_dev[b].p)))
+            return rc;
+        CHP_CUDA(ctx, cudaEventRecord(ctx->ev_consumed[b], ctx->stream));
+        if ((rc = launch((const int32_t*)ctx->unpack_dev[b].p, m))) return rc;
+    }
+    *bad = any_bad != 0;
+    return CHP_OK;
+}
+
 // Streams h_xy[0..n) into ctx->dl (accumulating; it must be initialised).
+// Inputs whose slots and y values fit 16 bits travel packed (half the PCIe
+// bytes) unless CHP_PIPELINE_NO_PACK is set in flags.
 int stream_reduce(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t width, int64_t q, int64_t x_off,
                   uint32_t flags) {
-    return stream_chunks(ctx, h_xy, n, [&](const int32_t* d, uint64_t m) {
+    auto launch = [&](const int32_t* d, uint64_t m) {
         return chp_reduce(ctx, d, m, width, q, x_off, (int32_t*)ctx->dl.p, flags | CHP_REDUCE_ACCUMULATE);
-    });
+    };
+    const bool packable = width <= 65536 && q >= 1 && q <= 65536 && !(flags & CHP_REDUCE_NO_VALIDATE) &&
+                          !(flags & CHP_PIPELINE_NO_PACK) && !std::getenv("CHP_PIPELINE_NO_PACK") &&
+                          x_off + 1 >= (int64_t)INT32_MIN &&
+                          x_off <= (int64_t)INT32_MAX;
+    if (!packable) return stream_chunks(ctx, h_xy, n, launch);
+    const uint32_t wcheck = (uint32_t)std::min<int64_t>(width, (int64_t)INT32_MAX - x_off);
+    bool bad = false;
+    int rc = stream_chunks_packed(ctx, h_xy, n, x_off, wcheck, (uint32_t)q, &bad, launch);
+    if (rc) return rc;
+    if (bad) {  // same outcome as the unpacked path: the error word of DL
+        int32_t minus1 = -1;
+        CHP_CUDA(ctx, cudaMemcpyAsync((int32_t*)ctx->dl.p + 2 * width, &minus1, 4, cudaMemcpyHostToDevice,
+                                      ctx->stream));
+        CHP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    }
+    return CHP_OK;
 }
 
 // Compaction (+ hull) of ctx->dl, then the requested outputs to the host.
@@ -174,7 +367,11 @@ void chp_ctx_destroy(chp_ctx* ctx) {
                       &ctx->filter, &ctx->sample, &ctx->gridbar, &ctx->dl, &ctx->counts, &ctx->chain, &ctx->lower, &ctx->upper,
                       &ctx->hull, &ctx->occ, &ctx->lpairs, &ctx->stage_dev[0], &ctx->stage_dev[1]};
     for (DevBuf* b : bufs) free_buf(*b);
+    free_buf(ctx->unpack_dev[0]);
+    free_buf(ctx->unpack_dev[1]);
+    delete static_cast<HostPool*>(ctx->pool);
     for (int b = 0; b < 2; ++b) {
+        if (ctx->pack_host[b]) cudaFreeHost(ctx->pack_host[b]);
         if (ctx->stage_host[b]) cudaFreeHost(ctx->stage_host[b]);
         if (ctx->ev_copied[b]) cudaEventDestroy(ctx->ev_copied[b]);
         if (ctx->ev_consumed[b]) cudaEventDestroy(ctx->ev_consumed[b]);
@@ -210,10 +407,13 @@ uint64_t chp_launch_count(const chp_ctx* ctx) { return ctx ? ctx->launches : 0; 
 
 const char* chp_last_variant(const chp_ctx* ctx) { return ctx ? ctx->variant : "none"; }
 
+uint64_t chp_last_h2d_bytes(const chp_ctx* ctx) { return ctx ? ctx->h2d_bytes : 0; }
+
 int chp_pipeline_host(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t width, int64_t q,
                       int32_t* h_Lpairs, uint64_t* h_occ, int32_t* h_chain, int64_t* h_s, int32_t* h_hull,
                       int64_t* h_h) {
     if (!ctx) return CHP_EINVAL;
+    ctx->h2d_bytes = 0;
     if (width < 1) return chp_einval(ctx, "reduce: width must be >= 1");
     if (width > (1ll << 29)) return chp_einval(ctx, "reduce: width exceeds the device limit 2^29");
     CHP_CUDA(ctx, cudaSetDevice(ctx->device));
@@ -227,6 +427,7 @@ int chp_pipeline_host(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t wid
 
 int chp_translate_host(chp_ctx* ctx, const int32_t* h_in, uint64_t n, int32_t dx, int32_t dy, int32_t* h_out) {
     if (!ctx) return CHP_EINVAL;
+    ctx->h2d_bytes = 0;
     if (n == 0) return CHP_OK;
     CHP_CUDA(ctx, cudaSetDevice(ctx->device));
     DevBuf buf;
@@ -247,6 +448,7 @@ int chp_translate_host(chp_ctx* ctx, const int32_t* h_in, uint64_t n, int32_t dx
 int chp_polyline_host(chp_ctx* ctx, const int32_t* h_Lpairs, int64_t width, int64_t major_off, int64_t minor_off,
                       int swapped, int32_t* h_chain, int64_t* h_s) {
     if (!ctx) return CHP_EINVAL;
+    ctx->h2d_bytes = 0;
     if (width < 1 || width > (1ll << 29)) return chp_einval(ctx, "build_polyline: width must be in [1, 2^29]");
     CHP_CUDA(ctx, cudaSetDevice(ctx->device));
     int rc;
@@ -275,6 +477,7 @@ int chp_polyline_host(chp_ctx* ctx, const int32_t* h_Lpairs, int64_t width, int6
 int chp_precondition_host(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t* h_bbox4, int32_t* h_Lpairs, int32_t* h_chain,
                           int64_t* h_s, int32_t* h_hull, int64_t* h_h) {
     if (!ctx) return CHP_EINVAL;
+    ctx->h2d_bytes = 0;
     if (n == 0) return chp_einval(ctx, "precondition: empty input");
     CHP_CUDA(ctx, cudaSetDevice(ctx->device));
     // Step 1 (bounds).  The points stay resident for step 3 when they fit a

@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <string>
+#include <utility>
 
 #include "chp_b200.h"
 
@@ -45,6 +46,13 @@ struct chp_ctx {
     size_t stage_bytes = 0;
     cudaEvent_t ev_copied[2] = {nullptr, nullptr};
     cudaEvent_t ev_consumed[2] = {nullptr, nullptr};
+    // Packed host pipeline: pinned 4-byte/point staging, unpacked device
+    // chunks, and a persistent host thread pool (abi.cu HostPool).
+    void* pack_host[2] = {nullptr, nullptr};
+    size_t pack_bytes = 0;
+    DevBuf unpack_dev[2];
+    void* pool = nullptr;
+    uint64_t h2d_bytes = 0;  // of the current / last host pipeline call
 };
 
 // Record the first CUDA error of a launch sequence in ctx->err.
@@ -87,6 +95,9 @@ static inline int chp_ensure(chp_ctx* ctx, DevBuf& b, size_t bytes) {
 // K0 pieces used by the host pipelines (misc.cu).
 int chp_bounds_init(chp_ctx* ctx, int32_t* d_out4);
 int chp_bounds_accumulate(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int32_t* d_out4);
+// Packed host pipeline (abi.cu): 32-bit words (slot | (y - 1) << 16) back to
+// int32 (x, y) pairs with x = slot + base.
+int chp_unpack16(chp_ctx* ctx, const uint32_t* d_in, uint64_t n, int32_t base, int32_t* d_out);
 
 // ----------------------------------------------------------- device side
 
@@ -106,6 +117,31 @@ __device__ __forceinline__ int2 ld_cg2(const int2* p) {
     return r;
 }
 // Fire-and-forget global min (SASS RED.MIN).
+// Programmatic dependent launch.  A kernel launched with launch_pdl may be
+// scheduled while its predecessor on the stream is still running; it must
+// call pdl_wait() before touching anything the predecessor writes (the wait
+// returns once that grid has completed and its writes are visible; it is a
+// no-op without the launch attribute).  pdl_trigger() lets the dependent be
+// scheduled before this grid ends.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                              Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 __device__ __forceinline__ void red_min(int* p, int v) {
     asm volatile("red.relaxed.gpu.global.min.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }

@@ -70,6 +70,7 @@ __global__ void __launch_bounds__(kCT) k_compact(const int* __restrict__ DL, uin
     __shared__ uint32_t s_tile;
     __shared__ unsigned long long s_warp[kCT / 32];
     __shared__ unsigned long long s_excl;
+    pdl_wait();  // DL from K1 (launched as a programmatic dependent)
     // Tile order: block index when every tile's CTA is co-resident (no
     // predecessor can be waiting for a slot), else an atomic ticket so that
     // a tile only starts after all its predecessors have.
@@ -265,11 +266,11 @@ extern "C" int chp_compact(chp_ctx* ctx, const int32_t* d_L, int64_t width, int6
     }
     const int use_ticket = ntiles > ctx->compact_resident ? 1 : 0;
     Map m{major_off, minor_off, swapped};
-    k_compact<<<ntiles, kCT, 0, ctx->stream>>>(
-        d_L, (uint32_t)width, m, reinterpret_cast<int2*>(d_chain), reinterpret_cast<unsigned long long*>(d_occ),
-        reinterpret_cast<int2*>(d_Lpairs), reinterpret_cast<int2*>(d_lower), reinterpret_cast<int2*>(d_upper),
-        reinterpret_cast<int2*>(d_upperd), reinterpret_cast<long long*>(d_counts), st_cur, st_next, ntiles,
-        use_ticket);
+    CHP_CUDA(ctx, launch_pdl(k_compact, dim3(ntiles), dim3(kCT), 0, ctx->stream, (const int*)d_L, (uint32_t)width, m,
+                             reinterpret_cast<int2*>(d_chain), reinterpret_cast<unsigned long long*>(d_occ),
+                             reinterpret_cast<int2*>(d_Lpairs), reinterpret_cast<int2*>(d_lower),
+                             reinterpret_cast<int2*>(d_upper), reinterpret_cast<int2*>(d_upperd),
+                             reinterpret_cast<long long*>(d_counts), st_cur, st_next, ntiles, use_ticket));
     CHP_LAUNCHED(ctx);
     ctx->status_clean[cur] = 0;         // dirty now
     ctx->status_clean[cur ^ 1] = ntiles;  // cleared by this launch

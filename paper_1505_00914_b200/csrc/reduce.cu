@@ -730,6 +730,7 @@ __global__ void __launch_bounds__(kThreads) k_sample_learn(const int32_t* __rest
                                                            int init_dl, int stages) {
     extern __shared__ uint4 smem4[];
     uint8_t* ring = reinterpret_cast<uint8_t*>(smem4) + table_span((size_t)wpad * 2);
+    pdl_trigger();  // the merge may queue (it cannot co-reside; it waits)
     sample_init(smem4, wpad, DL, width, init_dl);
     __syncthreads();
     sample_fold<TMA>(xy, n, g, width, ys, reinterpret_cast<uint16_t*>(smem4), ring, stages);
@@ -748,6 +749,8 @@ __global__ void __launch_bounds__(kMergeCols * kMergeSlices) k_sample_merge(cons
                                                                            uint32_t ntables, uint32_t width,
                                                                            uint32_t wpad, uint16_t* __restrict__ F) {
     __shared__ uint4 part[kMergeSlices][kMergeCols];
+    pdl_trigger();
+    pdl_wait();  // the sample tables
     const uint32_t chunk = blockIdx.x * kMergeCols + threadIdx.x;
     const uint32_t nchunks = wpad / 8;
     const uint4 ones = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
@@ -866,6 +869,8 @@ __global__ void __launch_bounds__(kThreads) k_reduce_sampled(const int32_t* __re
                                                              int* __restrict__ DL) {
     extern __shared__ uint4 smem4[];
     uint8_t* ring = reinterpret_cast<uint8_t*>(smem4) + table_span((size_t)wpad * 2);
+    pdl_trigger();
+    pdl_wait();  // the merged table (and DL, initialised by the sample pass)
     {
         const uint4* F4 = reinterpret_cast<const uint4*>(F);
         for (uint32_t i = threadIdx.x; i < wpad / 8; i += blockDim.x) smem4[i] = __ldcg(F4 + i);
@@ -1083,6 +1088,17 @@ int blocks_for(chp_ctx* ctx, const void* fn, size_t smem, int cap_per_sm) {
         CHP_CUDA((ctx), cudaFuncSetAttribute(fn_, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(plan).smem)); \
         const int blocks_ = blocks_for((ctx), (const void*)fn_, (plan).smem, 2);                        \
         fn_<<<blocks_, kThreads, (plan).smem, (ctx)->stream>>>(__VA_ARGS__);                            \
+        CHP_LAUNCHED(ctx);                                                                               \
+    } while (0)
+
+// As CHP_LAUNCH_PLANNED, launched as a programmatic dependent of the
+// previous kernel on the stream (the kernel calls pdl_wait()).
+#define CHP_LAUNCH_PLANNED_PDL(ctx, plan, KTMA, KREG, ...)                                               \
+    do {                                                                                                 \
+        auto fn_ = (plan).tma ? (KTMA) : (KREG);                                                         \
+        CHP_CUDA((ctx), cudaFuncSetAttribute(fn_, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(plan).smem)); \
+        const int blocks_ = blocks_for((ctx), (const void*)fn_, (plan).smem, 2);                        \
+        CHP_CUDA((ctx), launch_pdl(fn_, dim3(blocks_), dim3(kThreads), (plan).smem, (ctx)->stream, __VA_ARGS__)); \
         CHP_LAUNCHED(ctx);                                                                               \
     } while (0)
 
@@ -1305,13 +1321,14 @@ extern "C" int chp_reduce(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t
                 CHP_LAUNCHED(ctx);
             }
             const uint32_t nchunks = wpad8 / 8;
-            k_sample_merge<<<(nchunks + kMergeCols - 1) / kMergeCols, dim3(kMergeCols, kMergeSlices), 0,
-                             ctx->stream>>>((const uint16_t*)ctx->sample.p, sblocks, w, wpad8,
-                                            (uint16_t*)ctx->filter.p);
+            CHP_CUDA(ctx, launch_pdl(k_sample_merge, dim3((nchunks + kMergeCols - 1) / kMergeCols),
+                                     dim3(kMergeCols, kMergeSlices), 0, ctx->stream,
+                                     (const uint16_t*)ctx->sample.p, (uint32_t)sblocks, w, wpad8,
+                                     (uint16_t*)ctx->filter.p));
             CHP_LAUNCHED(ctx);
             const Plan pl = plan_for(ctx, tbytes, flags, false);
-            CHP_LAUNCH_PLANNED(ctx, pl, k_reduce_sampled<true>, k_reduce_sampled<false>, d_xy, n, g, w, wpad8, ys,
-                               (const uint16_t*)ctx->filter.p, pl.stages, d_L);
+            CHP_LAUNCH_PLANNED_PDL(ctx, pl, k_reduce_sampled<true>, k_reduce_sampled<false>, d_xy, n, g, w, wpad8,
+                                   ys, (const uint16_t*)ctx->filter.p, pl.stages, d_L);
             ctx->variant = "sampled";
             return CHP_OK;
         }

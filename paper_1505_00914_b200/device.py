@@ -78,6 +78,11 @@ class Context:
     def variant(self) -> str:
         return self.L.chp_last_variant(self.h).decode()
 
+    @property
+    def last_h2d_bytes(self) -> int:
+        """Host->device bytes of the last host-pipeline call (4/point when packed)."""
+        return int(self.L.chp_last_h2d_bytes(self.h))
+
     def dl_len(self, width: int) -> int:
         return int(self.L.chp_dl_len(int(width)))
 

@@ -45,3 +45,51 @@ def test_pipeline_host_invalid_point_raises(ctx):
     xy[16_777_300] = (65537, 5)  # in the second chunk
     with pytest.raises(ValueError):
         ctx.pipeline_host(xy, 65536, 65536)
+
+
+# The packed transfer (slot | (y - 1) << 16 words, 4 bytes per point) is taken
+# when width <= 2^16 and q <= 2^16; the int32 path otherwise.  Both must give
+# the same answers and the same errors.
+@pytest.mark.parametrize("n", [1, 3, 4, 5, 1001, 16_777_216 + 7])
+def test_pipeline_host_packed_sizes(ctx, orc, n):
+    p = 4096
+    xy = generate_host(2, 11, p, n)
+    out = ctx.pipeline_host(xy, p, p, L=True, chain=True)
+    assert ctx.last_h2d_bytes == 4 * n
+    ref = orc.pipeline(xy, p, p)
+    assert np.array_equal(out["L"], ref["L"])
+    assert np.array_equal(out["chain"], ref["chain"])
+
+
+def test_pipeline_host_unpacked_when_wide(ctx, orc):
+    p = 65536
+    xy = generate_host(2, 2, p, 100_000)
+    xy[:, 1] = xy[:, 1] * 2  # y up to 2^17: q > 2^16 -> int32 transfer
+    out = ctx.pipeline_host(xy, p, 2 * p, L=True, chain=True)
+    assert ctx.last_h2d_bytes == 8 * len(xy)
+    ref = orc.pipeline(xy, p, 2 * p)
+    assert np.array_equal(out["L"], ref["L"])
+    assert np.array_equal(out["chain"], ref["chain"])
+
+
+@pytest.mark.parametrize("bad", [(0, 5), (4097, 5), (7, 0), (7, 4097), (-2**31, 1), (2**31 - 1, 2**31 - 1)])
+@pytest.mark.parametrize("where", [0, 2, 999_999])
+def test_pipeline_host_packed_invalid_raises(ctx, bad, where):
+    p = 4096
+    xy = generate_host(2, 2, p, 1_000_000)
+    xy[where] = bad
+    with pytest.raises(ValueError):
+        ctx.pipeline_host(xy, p, p)
+    xy[where] = (1, 1)  # and the context is still usable afterwards
+    ctx.pipeline_host(xy, p, p)
+
+
+def test_pipeline_host_packed_extremes(ctx, orc):
+    # slots 0 and p-1, y = 1 and y = q: the 16-bit fields at both ends
+    p = 65536
+    xy = np.array([[1, 1], [1, 65536], [65536, 1], [65536, 65536], [300, 7]], np.int32)
+    xy = np.repeat(xy, 1000, axis=0)
+    out = ctx.pipeline_host(xy, p, p, L=True, chain=True)
+    ref = orc.pipeline(xy, p, p)
+    assert np.array_equal(out["L"], ref["L"])
+    assert np.array_equal(out["chain"], ref["chain"])
