@@ -54,7 +54,7 @@ def parse():
     ap.add_argument("--flags", type=int, default=0, help="chp_reduce flags (variant forcing, experiments)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     return ap.parse_args()
 
 
@@ -343,8 +343,10 @@ def main():
         h2d = ctx.last_h2d_bytes
         e2e = {"value": total_points / (e2e_ms * 1e-3) / 1e9, "unit": "Gpoints/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": int(s_out[0]) * 8 + 64, "ms_per_step": e2e_ms,
-               "path": "chp_pipeline_host (pinned int32 input; 16 Mi-point chunks, "
-                       + ("packed to 16-bit slot|y words on host threads, " if h2d < n * 8 else "")
+               "path": "chp_pipeline_host (pinned int32 input; "
+                       + ("4 Mi-point chunks packed to 16-bit slot|y words on host threads, int32 chunks "
+                          "DMA'd from the input's end while the host packs, " if h2d < n * 8 else
+                          "16 Mi-point int32 chunks, ")
                        + "H2D overlapped with K1)"}
         del host
 

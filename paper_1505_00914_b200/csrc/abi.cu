@@ -6,6 +6,7 @@
 // previous chunk on the compute stream (two device buffers, event-ordered),
 // then K3 (+K4) run on device and only L / the chain / the hull come back.
 #include <algorithm>
+#include <chrono>
 #include <condition_variable>
 #include <cstdlib>
 #include <cstring>
@@ -192,16 +193,30 @@ uint32_t pack16(const int32_t* __restrict__ src, uint32_t* __restrict__ dst, uin
 // of chunk k-1 is in flight, so PCIe carries half the bytes; on the device
 // k_unpack16 restores int32 pairs and launch() consumes them.  *bad is set
 // when any point is invalid (the caller fails the call).
+//
+// When the host packs slower than PCIe drains (measured: ~9 Gpts/s on 16
+// cores vs ~13.7 Gpts/s of packed words) and the input is pinned, the copy
+// engine would idle during each pack; it is kept busy with int32 chunks
+// DMA'd straight from the END of the input (K1 validates those itself), so
+// the packed front and the raw back meet where both resources finish.
 template <typename Launch>
 int stream_chunks_packed(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t x_off, uint32_t wcheck,
                          uint32_t qmax, bool* bad, Launch&& launch) {
     *bad = false;
     if (n == 0) return CHP_OK;
-    const uint64_t chunk = std::min<uint64_t>(kChunkPts, n);
+    constexpr uint64_t kPackChunk = 4ull << 20;  // 4 Mi points: fine-grained balancing
+    static const double kPcieBps = std::getenv("CHP_PCIE_BPS") ? std::atof(std::getenv("CHP_PCIE_BPS")) : 50e9;
+    const uint64_t chunk = std::min<uint64_t>(kPackChunk, n);
+    const bool hybrid = is_pinned(h_xy);
     int rc;
     for (int b = 0; b < 2; ++b) {
         if ((rc = chp_ensure(ctx, ctx->stage_dev[b], (size_t)chunk * 4))) return rc;
         if ((rc = chp_ensure(ctx, ctx->unpack_dev[b], (size_t)chunk * 8))) return rc;
+        if (hybrid && (rc = chp_ensure(ctx, ctx->raw_dev[b], (size_t)chunk * 8))) return rc;
+        if (hybrid && !ctx->ev_rcopied[b]) {
+            CHP_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_rcopied[b], cudaEventDisableTiming));
+            CHP_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_rconsumed[b], cudaEventDisableTiming));
+        }
     }
     if (ctx->pack_bytes < (size_t)chunk * 4) {
         for (int b = 0; b < 2; ++b) {
@@ -216,35 +231,74 @@ int stream_chunks_packed(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t 
     for (int b = 0; b < 2; ++b) {
         CHP_CUDA(ctx, cudaEventRecord(ctx->ev_consumed[b], ctx->stream));
         CHP_CUDA(ctx, cudaEventRecord(ctx->ev_copied[b], ctx->copy_stream));
+        if (hybrid) {
+            CHP_CUDA(ctx, cudaEventRecord(ctx->ev_rconsumed[b], ctx->stream));
+            CHP_CUDA(ctx, cudaEventRecord(ctx->ev_rcopied[b], ctx->copy_stream));
+        }
     }
     uint32_t any_bad = 0;
     std::vector<uint32_t> part_bad((size_t)pool->parts());
-    uint64_t k = 0;
-    for (uint64_t off = 0; off < n; off += chunk, ++k) {
-        const int b = (int)(k & 1);
-        const uint64_t m = std::min<uint64_t>(chunk, n - off);
-        // The DMA out of this staging buffer (chunk k-2) must have finished.
+    uint64_t front = 0, back = n;  // packed: [0, front); raw: [back, n)
+    uint64_t k = 0, kr = 0;
+    // Raw int32 chunks from the back covering `secs` of copy-engine time.
+    auto raw_fill = [&](double secs) -> int {
+        uint64_t want = (uint64_t)(secs * kPcieBps / 8);
+        while (want > 0 && back > front) {
+            const int rb = (int)(kr++ & 1);
+            const uint64_t m = std::min<uint64_t>({want, chunk, back - front});
+            const uint64_t off = back - m;
+            CHP_CUDA(ctx, cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_rconsumed[rb], 0));
+            CHP_CUDA(ctx, cudaMemcpyAsync(ctx->raw_dev[rb].p, h_xy + 2 * off, (size_t)m * 8, cudaMemcpyHostToDevice,
+                                          ctx->copy_stream));
+            ctx->h2d_bytes += (uint64_t)m * 8;
+            CHP_CUDA(ctx, cudaEventRecord(ctx->ev_rcopied[rb], ctx->copy_stream));
+            CHP_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_rcopied[rb], 0));
+            int r = launch((const int32_t*)ctx->raw_dev[rb].p, m);
+            if (r) return r;
+            CHP_CUDA(ctx, cudaEventRecord(ctx->ev_rconsumed[rb], ctx->stream));
+            back = off;
+            want -= m;
+        }
+        return CHP_OK;
+    };
+    double dma_ahead = 0;  // copy-engine seconds already queued when a pack starts
+    while (front < back) {
+        const uint64_t m = std::min<uint64_t>(chunk, back - front);
+        if (hybrid) {
+            // Keep the copy engine busy for the duration of this pack.
+            const double t_pack = (double)m / ctx->pack_rate;
+            if (t_pack > dma_ahead && (rc = raw_fill(t_pack - dma_ahead))) return rc;
+            if (front >= back) break;
+        }
+        const uint64_t mm = std::min<uint64_t>(m, back - front);
+        const int b = (int)(k++ & 1);
+        // The DMA out of this staging buffer (two packed chunks ago) must be done.
         CHP_CUDA(ctx, cudaEventSynchronize(ctx->ev_copied[b]));
         uint32_t* dst = static_cast<uint32_t*>(ctx->pack_host[b]);
-        const int32_t* src = h_xy + 2 * off;
+        const int32_t* src = h_xy + 2 * front;
         const int parts = pool->parts();
+        const auto t0 = std::chrono::steady_clock::now();
         pool->run([&](int i) {
-            const uint64_t lo = (m * (uint64_t)i / parts) & ~3ull;
-            const uint64_t hi = i + 1 == parts ? m : (m * (uint64_t)(i + 1) / parts) & ~3ull;
+            const uint64_t lo = (mm * (uint64_t)i / parts) & ~3ull;
+            const uint64_t hi = i + 1 == parts ? mm : (mm * (uint64_t)(i + 1) / parts) & ~3ull;
             part_bad[(size_t)i] = pack16(src + 2 * lo, dst + lo, hi - lo, base, wcheck, qmax);
         });
+        const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (mm >= (1u << 20) && dt > 0) ctx->pack_rate = 0.5 * ctx->pack_rate + 0.5 * (double)mm / dt;
         for (uint32_t v : part_bad) any_bad |= v;
         CHP_CUDA(ctx, cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_consumed[b], 0));
-        CHP_CUDA(ctx, cudaMemcpyAsync(ctx->stage_dev[b].p, dst, (size_t)m * 4, cudaMemcpyHostToDevice,
+        CHP_CUDA(ctx, cudaMemcpyAsync(ctx->stage_dev[b].p, dst, (size_t)mm * 4, cudaMemcpyHostToDevice,
                                       ctx->copy_stream));
-        ctx->h2d_bytes += (uint64_t)m * 4;
+        ctx->h2d_bytes += (uint64_t)mm * 4;
+        dma_ahead = (double)mm * 4 / kPcieBps;
         CHP_CUDA(ctx, cudaEventRecord(ctx->ev_copied[b], ctx->copy_stream));
         CHP_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_copied[b], 0));
-        if ((rc = chp_unpack16(ctx, (const uint32_t*)ctx->stage_dev[b].p, m, (int32_t)base,
+        if ((rc = chp_unpack16(ctx, (const uint32_t*)ctx->stage_dev[b].p, mm, (int32_t)base,
                                (int32_t*)ctx->unpack_dev[b].p)))
             return rc;
         CHP_CUDA(ctx, cudaEventRecord(ctx->ev_consumed[b], ctx->stream));
-        if ((rc = launch((const int32_t*)ctx->unpack_dev[b].p, m))) return rc;
+        if ((rc = launch((const int32_t*)ctx->unpack_dev[b].p, mm))) return rc;
+        front += mm;
     }
     *bad = any_bad != 0;
     return CHP_OK;
@@ -369,6 +423,12 @@ void chp_ctx_destroy(chp_ctx* ctx) {
     for (DevBuf* b : bufs) free_buf(*b);
     free_buf(ctx->unpack_dev[0]);
     free_buf(ctx->unpack_dev[1]);
+    free_buf(ctx->raw_dev[0]);
+    free_buf(ctx->raw_dev[1]);
+    for (int b = 0; b < 2; ++b) {
+        if (ctx->ev_rcopied[b]) cudaEventDestroy(ctx->ev_rcopied[b]);
+        if (ctx->ev_rconsumed[b]) cudaEventDestroy(ctx->ev_rconsumed[b]);
+    }
     delete static_cast<HostPool*>(ctx->pool);
     for (int b = 0; b < 2; ++b) {
         if (ctx->pack_host[b]) cudaFreeHost(ctx->pack_host[b]);

@@ -53,6 +53,12 @@ struct chp_ctx {
     DevBuf unpack_dev[2];
     void* pool = nullptr;
     uint64_t h2d_bytes = 0;  // of the current / last host pipeline call
+    // Hybrid packed pipeline: int32 chunks DMA'd straight from a pinned input
+    // while the host packs (abi.cu), and the measured host pack rate.
+    DevBuf raw_dev[2];
+    cudaEvent_t ev_rcopied[2] = {nullptr, nullptr};
+    cudaEvent_t ev_rconsumed[2] = {nullptr, nullptr};
+    double pack_rate = 8e9;  // points / s
 };
 
 // Record the first CUDA error of a launch sequence in ctx->err.

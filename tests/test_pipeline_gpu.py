@@ -50,12 +50,25 @@ def test_pipeline_host_invalid_point_raises(ctx):
 # The packed transfer (slot | (y - 1) << 16 words, 4 bytes per point) is taken
 # when width <= 2^16 and q <= 2^16; the int32 path otherwise.  Both must give
 # the same answers and the same errors.
+def _pinned(xy):
+    t = torch.empty(xy.shape, dtype=torch.int32, pin_memory=True)
+    t.copy_(torch.from_numpy(xy))
+    return t.numpy()
+
+
 @pytest.mark.parametrize("n", [1, 3, 4, 5, 1001, 16_777_216 + 7])
-def test_pipeline_host_packed_sizes(ctx, orc, n):
+@pytest.mark.parametrize("pinned", [False, True])
+def test_pipeline_host_packed_sizes(ctx, orc, n, pinned):
+    # pinned input: the hybrid form (packed front + int32 chunks from the back)
     p = 4096
     xy = generate_host(2, 11, p, n)
+    if pinned:
+        xy = _pinned(xy)
     out = ctx.pipeline_host(xy, p, p, L=True, chain=True)
-    assert ctx.last_h2d_bytes == 4 * n
+    if pinned:
+        assert 4 * n <= ctx.last_h2d_bytes <= 8 * n
+    else:
+        assert ctx.last_h2d_bytes == 4 * n
     ref = orc.pipeline(xy, p, p)
     assert np.array_equal(out["L"], ref["L"])
     assert np.array_equal(out["chain"], ref["chain"])
@@ -74,9 +87,12 @@ def test_pipeline_host_unpacked_when_wide(ctx, orc):
 
 @pytest.mark.parametrize("bad", [(0, 5), (4097, 5), (7, 0), (7, 4097), (-2**31, 1), (2**31 - 1, 2**31 - 1)])
 @pytest.mark.parametrize("where", [0, 2, 999_999])
-def test_pipeline_host_packed_invalid_raises(ctx, bad, where):
+@pytest.mark.parametrize("pinned", [False, True])
+def test_pipeline_host_packed_invalid_raises(ctx, bad, where, pinned):
     p = 4096
     xy = generate_host(2, 2, p, 1_000_000)
+    if pinned:
+        xy = _pinned(xy)
     xy[where] = bad
     with pytest.raises(ValueError):
         ctx.pipeline_host(xy, p, p)
