@@ -157,9 +157,18 @@ __global__ void __launch_bounds__(kCT) k_compact(const int* __restrict__ DL, uin
                     idx[k] = top - lane - 32 * k;
                     st[k] = idx[k] >= 0 ? ld_acquire(status + idx[k]) : kFlagIncl;
                 }
+                // Re-poll every not-yet-published predecessor together, one
+                // round trip per pass (a per-slot spin serialised up to 8
+                // L2 round trips per lane: the look-back took ~6 us at C2).
+                for (;;) {
+                    uint32_t pending = 0;
 #pragma unroll
-                for (int k = 0; k < kPer; ++k)
-                    while ((st[k] >> 62) == 0) st[k] = ld_acquire(status + idx[k]);
+                    for (int k = 0; k < kPer; ++k) pending |= (uint32_t)((st[k] >> 62) == 0) << k;
+                    if (!__any_sync(0xffffffffu, pending != 0)) break;
+#pragma unroll
+                    for (int k = 0; k < kPer; ++k)
+                        if ((pending >> k) & 1) st[k] = ld_acquire(status + idx[k]);
+                }
                 long long best = LLONG_MIN;  // nearest inclusive predecessor in the window
 #pragma unroll
                 for (int k = 0; k < kPer; ++k)
