@@ -33,6 +33,10 @@ def build(ref: bool | None = None) -> None:
         ref = os.path.isdir(REF_SRC)
     if ref:
         targets.append("ref")
+        # the reference's acceptance suite linked to the device drop-in
+        # (needs the built library; tests/test_acceptance_gpu.py runs it)
+        if os.path.exists(os.path.join(HERE, "..", "paper_1505_00914_b200", "lib", "libchp_b200.so")):
+            targets.append("acceptance")
     subprocess.run(["make", "-s", "-C", HERE] + targets, check=True)
 
 

@@ -1,0 +1,28 @@
+"""The reference's own acceptance suite (proj/tests/acceptance.cpp, ten
+criteria) built against this repo's drop-in headers and linked to
+libchp_b200.so (oracle/Makefile target `acceptance`): reducer::precondition,
+valid_points, hulls::melkman and the geometry helpers run on the device,
+while the comparison hulls it checks against (brute_force_hull, graham_scan,
+quickhull, jarvis_march) are the reference's own CPU code.  Criterion 1
+compares the device-reduced hull with the reference's brute-force oracle on
+10,000 mixed sets; criterion 2 the device Melkman with the reference's three
+other hulls on 1,000 sets of up to 1e5 points."""
+import os
+import subprocess
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+BIN = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref",
+                   "acceptance_dropin")
+
+
+@pytest.mark.skipif(not os.path.exists(BIN), reason="built only where /root/reference is present")
+def test_reference_acceptance_suite_on_dropin():
+    r = subprocess.run([BIN], capture_output=True, text=True, timeout=900)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out
+    assert "all criteria passed" in out, out
+    for k in range(1, 11):
+        assert f"criterion {k} (" in out and "FAIL" not in out, out
