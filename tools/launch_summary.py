@@ -39,14 +39,21 @@ def main():
     for d in step:
         t = d.get("gpu__time_duration.sum", 0)
         b = d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0)
-        out.append({"kernel": d["kernel"], "us": round(t / 1e3, 2), "dram_bytes": int(b),
-                    "share": round(t / tot, 3)})
+        e = {"kernel": d["kernel"], "us": round(t / 1e3, 2), "dram_bytes": int(b), "share": round(t / tot, 3)}
+        for key, name in (("dram__throughput.avg.pct_of_peak_sustained_elapsed", "dram_pct"),
+                          ("lts__t_requests_srcunit_tex_op_red.sum", "global_red_requests"),
+                          ("lts__t_requests_srcunit_tex_op_atom.sum", "global_atom_requests"),
+                          ("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum", "smem_atom_wavefronts")):
+            if key in d:
+                e[name] = round(d[key], 1) if name == "dram_pct" else int(d[key])
+        out.append(e)
     k1 = [d for d in out if not d["kernel"].startswith("k_compact")]
     k1_bytes = sum(d["dram_bytes"] for d in k1)
     summary = {
         "config": config, "n": n,
-        "source": "ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
-                  "--clock-control none over bench.py --steps 1 (cold, serialised launches: use the shares)",
+        "source": "ncu --metrics gpu__time_duration.sum, dram__bytes_read/write.sum, dram__throughput pct, "
+                  "lts red/atom requests, smem atom wavefronts --clock-control none over bench.py --steps 1 "
+                  "(cold, serialised launches: use the shares)",
         "step_launches": out, "step_us_sum": round(tot / 1e3, 1),
         "k1_share": round(sum(d["us"] for d in k1) * 1e3 / tot, 3),
         "k1_dram_bytes_per_call": k1_bytes, "algorithmic_bytes_per_call": 8 * n,

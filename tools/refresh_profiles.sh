@@ -11,7 +11,7 @@ out=gpurun_out
 declare -A N=([2]=100000000 [3]=1000000000 [4]=1000000000 [5]=4000000000)
 for c in ${CONFIGS:-2 3 4 5}; do
   if timeout 600 python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > $out/pre_c$c.json 2> $out/pre_c$c.err; then
-    timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+    timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,dram__throughput.avg.pct_of_peak_sustained_elapsed,lts__t_requests_srcunit_tex_op_red.sum,lts__t_requests_srcunit_tex_op_atom.sum,l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum --clock-control none \
        -c 80 --csv --log-file $out/launches_c$c.csv \
        python bench.py --config $c --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > $out/ncu_c$c.log 2>&1 \
        && python tools/launch_summary.py $out/launches_c$c.csv $c ${N[$c]} $rnd > /dev/null \
