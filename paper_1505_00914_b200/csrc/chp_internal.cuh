@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <string>
+#include <unordered_map>
 #include <utility>
 
 #include "chp_b200.h"
@@ -59,6 +60,9 @@ struct chp_ctx {
     cudaEvent_t ev_rcopied[2] = {nullptr, nullptr};
     cudaEvent_t ev_rconsumed[2] = {nullptr, nullptr};
     double pack_rate = 8e9;  // points / s
+    // Launch-setup cache (reduce.cu kernel_blocks): kernel -> (dynamic smem
+    // it was configured for, resident blocks per SM at that size).
+    std::unordered_map<const void*, std::pair<size_t, int>> kcache;
 };
 
 // Record the first CUDA error of a launch sequence in ctx->err.

@@ -1073,20 +1073,33 @@ Plan plan_for(const chp_ctx* ctx, size_t table_bytes, uint32_t flags, bool tma_d
     return p;
 }
 
-int blocks_for(chp_ctx* ctx, const void* fn, size_t smem, int cap_per_sm) {
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, smem);
+// Grid size for a kThreads kernel with `smem` dynamic shared memory, setting
+// the kernel's smem attribute first.  Cached per context: the attribute call
+// and the occupancy query cost microseconds of host time per launch, which
+// the bench's launch rate (4 launches per 0.17 ms step) notices.
+int kernel_blocks(chp_ctx* ctx, const void* fn, size_t smem, int cap_per_sm, int* blocks) {
+    auto it = ctx->kcache.find(fn);
+    int per_sm;
+    if (it != ctx->kcache.end() && it->second.first == smem) {
+        per_sm = it->second.second;
+    } else {
+        CHP_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        per_sm = 0;
+        CHP_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, smem));
+        ctx->kcache[fn] = {smem, per_sm};
+    }
     if (per_sm < 1) per_sm = 1;
     if (per_sm > cap_per_sm) per_sm = cap_per_sm;
-    return per_sm * ctx->sm_count;
+    *blocks = per_sm * ctx->sm_count;
+    return CHP_OK;
 }
 
 // Launches kernel template K<..., TMA> with the plan's dynamic shared memory.
 #define CHP_LAUNCH_PLANNED(ctx, plan, KTMA, KREG, ...)                                                   \
     do {                                                                                                 \
         auto fn_ = (plan).tma ? (KTMA) : (KREG);                                                         \
-        CHP_CUDA((ctx), cudaFuncSetAttribute(fn_, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(plan).smem)); \
-        const int blocks_ = blocks_for((ctx), (const void*)fn_, (plan).smem, 2);                        \
+        int blocks_ = 0;                                                                                 \
+        if (int rc_ = kernel_blocks((ctx), (const void*)fn_, (plan).smem, 2, &blocks_)) return rc_;     \
         fn_<<<blocks_, kThreads, (plan).smem, (ctx)->stream>>>(__VA_ARGS__);                            \
         CHP_LAUNCHED(ctx);                                                                               \
     } while (0)
@@ -1096,8 +1109,8 @@ int blocks_for(chp_ctx* ctx, const void* fn, size_t smem, int cap_per_sm) {
 #define CHP_LAUNCH_PLANNED_PDL(ctx, plan, KTMA, KREG, ...)                                               \
     do {                                                                                                 \
         auto fn_ = (plan).tma ? (KTMA) : (KREG);                                                         \
-        CHP_CUDA((ctx), cudaFuncSetAttribute(fn_, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(plan).smem)); \
-        const int blocks_ = blocks_for((ctx), (const void*)fn_, (plan).smem, 2);                        \
+        int blocks_ = 0;                                                                                 \
+        if (int rc_ = kernel_blocks((ctx), (const void*)fn_, (plan).smem, 2, &blocks_)) return rc_;     \
         CHP_CUDA((ctx), launch_pdl(fn_, dim3(blocks_), dim3(kThreads), (plan).smem, (ctx)->stream, __VA_ARGS__)); \
         CHP_LAUNCHED(ctx);                                                                               \
     } while (0)
@@ -1315,7 +1328,8 @@ extern "C" int chp_reduce(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t
             {
                 const Plan sp = plan_for(ctx, tbytes, (flags & CHP_REDUCE_SAMPLE_TMA) ? CHP_REDUCE_TMA : 0u, false);
                 auto fn = sp.tma ? k_sample_learn<true> : k_sample_learn<false>;
-                CHP_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp.smem));
+                int unused = 0;
+                if ((rc = kernel_blocks(ctx, (const void*)fn, sp.smem, 1, &unused))) return rc;
                 fn<<<sblocks, kThreads, sp.smem, ctx->stream>>>(d_xy, ns, g, w, wpad8, ys, (uint16_t*)ctx->sample.p,
                                                                 d_L, need_init ? 1 : 0, sp.stages);
                 CHP_LAUNCHED(ctx);
