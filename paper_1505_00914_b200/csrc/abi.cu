@@ -156,7 +156,7 @@ int stream_chunks(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, Launch&& launch
 // outside [1, q]).  SSE2, 4 points per step, non-temporal stores: the pinned
 // staging is only read by the DMA engine, so skipping the read-for-ownership
 // saves a third of the host memory traffic.
-uint32_t pack16(const int32_t* __restrict__ src, uint32_t* __restrict__ dst, uint64_t m, uint32_t base,
+uint32_t pack16_sse2(const int32_t* __restrict__ src, uint32_t* __restrict__ dst, uint64_t m, uint32_t base,
                 uint32_t wcheck, uint32_t qmax) {
     uint32_t bad = 0;
     uint64_t i = 0;
@@ -188,14 +188,58 @@ uint32_t pack16(const int32_t* __restrict__ src, uint32_t* __restrict__ dst, uin
     return bad | (uint32_t)(_mm_movemask_epi8(okv) != 0xFFFF);
 }
 
+// AVX2 form (8 points per step): tools/micro_pack.cpp measured 11.7 vs 9.5
+// Gpts/s for SSE2 on the 16-core GPU host.  Unsigned range checks as
+// max_epu32(v, lim) == v  <=>  v >= lim.
+__attribute__((target("avx2"))) uint32_t pack16_avx2(const int32_t* __restrict__ src, uint32_t* __restrict__ dst,
+                                                     uint64_t m, uint32_t base, uint32_t wcheck, uint32_t qmax) {
+    uint64_t i = 0;
+    uint32_t bad = 0;
+    for (; i < m && (reinterpret_cast<uintptr_t>(dst + i) & 31); ++i) {
+        const uint32_t s = (uint32_t)src[2 * i] - base;
+        const uint32_t ym1 = (uint32_t)src[2 * i + 1] - 1u;
+        bad |= (uint32_t)(s >= wcheck) | (uint32_t)(ym1 >= qmax);
+        dst[i] = s | (ym1 << 16);
+    }
+    const __m256i vbase = _mm256_set1_epi32((int)base), vone = _mm256_set1_epi32(1);
+    const __m256i wl = _mm256_set1_epi32((int)wcheck), ql = _mm256_set1_epi32((int)qmax);
+    const __m256i perm = _mm256_setr_epi32(0, 2, 4, 6, 1, 3, 5, 7);
+    __m256i badv = _mm256_setzero_si256();
+    for (; i + 8 <= m; i += 8) {
+        // x0 y0 .. x3 y3 | x4 y4 .. x7 y7 -> x0..x3 y0..y3 | x4..x7 y4..y7
+        const __m256i a = _mm256_permutevar8x32_epi32(_mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + 2 * i)), perm);
+        const __m256i b =
+            _mm256_permutevar8x32_epi32(_mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + 2 * i + 8)), perm);
+        const __m256i s = _mm256_sub_epi32(_mm256_permute2x128_si256(a, b, 0x20), vbase);
+        const __m256i ym1 = _mm256_sub_epi32(_mm256_permute2x128_si256(a, b, 0x31), vone);
+        badv = _mm256_or_si256(badv, _mm256_cmpeq_epi32(_mm256_max_epu32(s, wl), s));
+        badv = _mm256_or_si256(badv, _mm256_cmpeq_epi32(_mm256_max_epu32(ym1, ql), ym1));
+        _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + i), _mm256_or_si256(s, _mm256_slli_epi32(ym1, 16)));
+    }
+    for (; i < m; ++i) {
+        const uint32_t s = (uint32_t)src[2 * i] - base;
+        const uint32_t ym1 = (uint32_t)src[2 * i + 1] - 1u;
+        bad |= (uint32_t)(s >= wcheck) | (uint32_t)(ym1 >= qmax);
+        dst[i] = s | (ym1 << 16);
+    }
+    _mm_sfence();
+    return bad | (uint32_t)!_mm256_testz_si256(badv, badv);
+}
+
+uint32_t pack16(const int32_t* src, uint32_t* dst, uint64_t m, uint32_t base, uint32_t wcheck, uint32_t qmax) {
+    static const bool avx2 = __builtin_cpu_supports("avx2");
+    return avx2 ? pack16_avx2(src, dst, m, base, wcheck, qmax) : pack16_sse2(src, dst, m, base, wcheck, qmax);
+}
+
 // Packed form of stream_chunks for width <= 2^16 and 1 <= y <= q <= 2^16:
 // host workers pack chunk k into pinned 4-byte/point staging while the DMA
 // of chunk k-1 is in flight, so PCIe carries half the bytes; on the device
 // k_unpack16 restores int32 pairs and launch() consumes them.  *bad is set
 // when any point is invalid (the caller fails the call).
 //
-// When the host packs slower than PCIe drains (measured: ~9 Gpts/s on 16
-// cores vs ~13.7 Gpts/s of packed words) and the input is pinned, the copy
+// When the host packs slower than PCIe drains (16-core host: ~9-12 Gpts/s,
+// bound by host memory bandwidth once the DMA reads compete, vs ~13.7 Gpts/s
+// of packed words) and the input is pinned, the copy
 // engine would idle during each pack; it is kept busy with int32 chunks
 // DMA'd straight from the END of the input (K1 validates those itself), so
 // the packed front and the raw back meet where both resources finish.
@@ -204,8 +248,10 @@ int stream_chunks_packed(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t 
                          uint32_t qmax, bool* bad, Launch&& launch) {
     *bad = false;
     if (n == 0) return CHP_OK;
-    constexpr uint64_t kPackChunk = 4ull << 20;  // 4 Mi points: fine-grained balancing
-    static const double kPcieBps = std::getenv("CHP_PCIE_BPS") ? std::atof(std::getenv("CHP_PCIE_BPS")) : 50e9;
+    // 8 Mi points per chunk (e2e C2, hybrid: 2 Mi 8.7-9.1, 4 Mi 9.4-9.7, 8 Mi
+    // 9.9, 16 Mi 10.0 Gpts/s; smaller chunks pay the per-chunk dispatch).
+    constexpr uint64_t kPackChunk = 8ull << 20;
+    constexpr double kPcieBps = 50e9;  // H2D bytes / s (PCIe 5 x16, measured ~55e9)
     const uint64_t chunk = std::min<uint64_t>(kPackChunk, n);
     const bool hybrid = is_pinned(h_xy);
     int rc;
@@ -279,8 +325,8 @@ int stream_chunks_packed(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t 
         const int parts = pool->parts();
         const auto t0 = std::chrono::steady_clock::now();
         pool->run([&](int i) {
-            const uint64_t lo = (mm * (uint64_t)i / parts) & ~3ull;
-            const uint64_t hi = i + 1 == parts ? mm : (mm * (uint64_t)(i + 1) / parts) & ~3ull;
+            const uint64_t lo = (mm * (uint64_t)i / parts) & ~7ull;
+            const uint64_t hi = i + 1 == parts ? mm : (mm * (uint64_t)(i + 1) / parts) & ~7ull;
             part_bad[(size_t)i] = pack16(src + 2 * lo, dst + lo, hi - lo, base, wcheck, qmax);
         });
         const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
