@@ -353,7 +353,7 @@ def main():
         e2e = {"value": total_points / (e2e_ms * 1e-3) / 1e9, "unit": "Gpoints/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": int(s_out[0]) * 8 + 64, "ms_per_step": e2e_ms,
                "path": "chp_pipeline_host (pinned int32 input; "
-                       + ("4 Mi-point chunks packed to 16-bit slot|y words on host threads, int32 chunks "
+                       + ("8 Mi-point chunks packed to 16-bit slot|y words on host threads (AVX2), int32 chunks "
                           "DMA'd from the input's end while the host packs, " if h2d < n * 8 else
                           "16 Mi-point int32 chunks, ")
                        + "H2D overlapped with K1)"}
