@@ -28,7 +28,8 @@ def main():
         d = launches.setdefault(key, {"kernel": r[ix["Kernel Name"]].split("(")[0].replace("<unnamed>::", "")
                                       .replace("void ", "")})
         d[r[ix["Metric Name"]]] = float(r[ix["Metric Value"]].replace(",", ""))
-    seq = list(launches.values())
+    # only this repo's kernels (bench.py's pre-timing torch sleep kernel is not part of a step)
+    seq = [d for d in launches.values() if d["kernel"].startswith("k_")]
     # the last compaction that directly follows K1 (bench.py's hull leg compacts again)
     last = max(i for i, d in enumerate(seq)
                if d["kernel"].startswith("k_compact") and i > 0 and not seq[i - 1]["kernel"].startswith("k_compact"))
