@@ -28,6 +28,7 @@
 // flagged by a min-combined error word (DL[2*width]); the host turns it into
 // std::invalid_argument like the reference's validation loop (:175-178).
 #include <algorithm>
+#include <cstdlib>
 
 #include "chp_internal.cuh"
 #include "stream.cuh"
@@ -1130,12 +1131,20 @@ int run_group_filter(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, const Geo& g
     int rc = chp_ensure(ctx, ctx->filter, (size_t)(ngroups + 1) * sizeof(W) + 16);
     if (rc) return rc;
     const Plan pl = plan_for(ctx, (size_t)(ngroups + 1) * sizeof(W), flags, false);
-    // Misses RED (one-sided where the word allows) without reading the slot:
-    // with the doubling schedule the misses are few, and a warp that waits
-    // on an L2 read per miss group stalls the stream (C4: 471 vs 388 Gpts/s).
-    const bool read_first = (flags & CHP_REDUCE_MISS_READ) != 0;
+    // Miss handling per phase.  While the snapshots are young (phases that
+    // start before n/8) misses are frequent and mostly NOT improvements, so
+    // a miss reads its slot first and REDs only a real update (the REDs of
+    // those phases were contended: 8 M per phase at 35-110 G/s).  Later the
+    // misses are few and a read would stall the warp, so they RED one-sided
+    // without reading.  C4: read-first throughout 388, RED-only 488, this
+    // split 530 Gpts/s.  CHP_REDUCE_MISS_READ / _MISS_RED force one policy.
+    const bool force_read = (flags & CHP_REDUCE_MISS_READ) != 0;
+    const bool force_red = (flags & CHP_REDUCE_MISS_RED) != 0 && !force_read;
+    const uint64_t read_until = n >> 3;
+    uint64_t cur_done = 0;  // first point of the phase being launched
     auto pass = [&](const int32_t* xy, uint64_t cnt, const W* F) {
-        if (read_first)
+        const bool rf = force_read || (!force_red && cur_done < read_until);
+        if (rf)
             CHP_LAUNCH_PLANNED(ctx, pl, (k_reduce_filter<W, true, true>), (k_reduce_filter<W, true, false>), xy, cnt,
                                g, w, gshift, ys, F, ngroups, pl.stages, d_L);
         else
@@ -1158,6 +1167,7 @@ int run_group_filter(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, const Geo& g
                                                                             (W*)ctx->filter.p, ngroups);
         CHP_LAUNCHED(ctx);
         const uint64_t stop = std::min<uint64_t>(n, 2 * done);
+        cur_done = done;
         if ((rc = pass(d_xy + 2 * done, stop - done, (const W*)ctx->filter.p))) return rc;
         done = stop;
     }
