@@ -1152,13 +1152,14 @@ int run_group_filter(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, const Geo& g
                                cnt, g, w, gshift, ys, F, ngroups, pl.stages, d_L);
         return CHP_OK;
     };
-    // Phases double in length: warm-up n/2^kw (default n/256) with an empty
+    // Phases double in length: warm-up n/2^kw (default n/64) with an empty
     // table, then [d, 2d) against a snapshot of DL taken at d.  The snapshot
     // at d leaves ~1/d of the later points outside the band (SURVEY-style
     // simulation of C4: group hit rate 53% at n/64, 94% at n/7, 98% at n/2),
     // so doubling keeps the misses of every phase about equal.
     const uint32_t kfield = (flags >> 16) & 7;
-    const uint32_t kw = kfield ? kfield + 3 : 8;  // C4: kw 8 471, 9 464, 10 462 Gpts/s
+    // C4 with the read-first young phases: kw 4 525, 6 537, 7 534, 9 501 Gpts/s
+    const uint32_t kw = kfield ? kfield + 3 : 6;
     // (Inputs under 4 Mi points: one pass with the empty table.)
     const uint64_t warm = n < (1ull << 22) ? n : (n >> kw) & ~1ull;
     if ((rc = pass(d_xy, warm, nullptr))) return rc;
