@@ -9,24 +9,29 @@
 //            (lo, ~hi); read-compare-then-ATOMS, so a point that changes
 //            nothing costs one LDS.64.  Flushed to the global DL at the end
 //            with RED.MIN only where the CTA's value beats the global one.
-//  smem16  : same with both extremes of a slot packed into one 32-bit word
-//            (lo - ybase, 0xFFFF - (hi - ybase)) when the y range spans at
-//            most 2^16 values; updates by CAS (rare, filtered).  Twice the
-//            columns per CTA, twice the CTAs per SM.
-//  global  : any p; the slot table lives in the (L2-resident) global DL,
-//            read-compare-then-RED.MIN.
+//  smem16  : both extremes of a slot packed into one 32-bit word
+//            (y-1, 0xFFFF-(y-1)) minima when 1 <= y <= q <= 2^16; the hit
+//            test is one VIMNMX.U16x2, updates by CAS (rare).
+//  sampled : mid-size p: a per-column 8-bit strict-interior filter learned
+//            from an n/8 sample (racy per-CTA tables, byte-wise min merge),
+//            then one pass over all points; a miss REDs one side.
 //  filter  : any p; each CTA stages a conservative, quantised snapshot of
-//            the DL (per column group, 16-bit bounds) in shared memory and
-//            only points outside it touch L2 (read-compare-RED).  A point
-//            inside [flo, fhi] of its group cannot change its column: flo is
-//            an upper bound of every lo in the group, fhi a lower bound of
-//            every hi, and those only move outwards.
+//            the DL per column group in shared memory, rebuilt between
+//            phases of doubling length; only points outside it touch L2
+//            (read-compare-RED while the snapshots are young, one-sided RED
+//            after).  A point inside [flo, fhi] of its group cannot change
+//            its column: flo bounds every lo in the group from above, fhi
+//            every hi from below, and those only move outwards.
+//  global  : any p, no y bound; the slot table lives in the (L2-resident)
+//            global DL, read-compare-then-RED.MIN.
 //
 // Every variant streams the points once with 128-bit non-allocating loads
-// (2 points per load, 4 loads in flight per thread) over a persistent grid
-// sized from the occupancy calculator.  Out-of-range points are skipped and
-// flagged by a min-combined error word (DL[2*width]); the host turns it into
+// (2 points per load, software-pipelined) over a persistent grid sized from
+// the occupancy calculator.  Out-of-range points are flagged by a
+// min-combined error word (DL[2*width]); the host turns it into
 // std::invalid_argument like the reference's validation loop (:175-178).
+// In smem16/sampled/filter the validation is folded into the miss path
+// (DESIGN.md §3).
 #include <algorithm>
 #include <cstdlib>
 
@@ -1296,7 +1301,7 @@ extern "C" int chp_reduce(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t
             return CHP_OK;
         }
         case V_SAMPLED: {
-            // Sample pass (prefix n/16) -> merged strict-interior table -> one
+            // Sample pass (prefix n/8) -> merged strict-interior table -> one
             // pass over all n points.
             uint32_t ys = 0;
             while ((uint64_t)(q - 1) >> ys > 254) ++ys;
