@@ -30,8 +30,8 @@
 // the occupancy calculator.  Out-of-range points are flagged by a
 // min-combined error word (DL[2*width]); the host turns it into
 // std::invalid_argument like the reference's validation loop (:175-178).
-// In smem16/sampled/filter the validation is folded into the miss path
-// (DESIGN.md §3).
+// In sampled/filter the validation is folded into the miss path (DESIGN.md
+// §3); smem16 checks each point branch-free (two compares, a select).
 #include <algorithm>
 #include <cstdlib>
 
