@@ -28,6 +28,7 @@
  *   chp_pipeline_host     reduce + build_polyline (+ melkman) from HOST buffers, the drop-in's
  *                         workhorse (src/reducer.cpp:172-182, :211-222; src/hulls.cpp:396-440)
  *   chp_precondition_host chp::reducer::precondition    include/chp/reducer.hpp:100-101,
+ *   chp_precondition_run  (one-pass form of the above, outputs via chp_last_outputs)
  *                                                       src/reducer.cpp:235-281
  */
 #ifndef CHP_B200_H
@@ -191,6 +192,16 @@ int chp_polyline_host(chp_ctx* ctx, const int32_t* h_Lpairs, int64_t width,
 int chp_precondition_host(chp_ctx* ctx, const int32_t* h_xy, uint64_t n,
                           int64_t* h_bbox4, int32_t* h_Lpairs, int32_t* h_chain,
                           int64_t* h_s, int32_t* h_hull, int64_t* h_h);
+
+/* The same in ONE pass over the input when the width is not known up
+ * front: bounds, K1, K3 (and K4 when want_hull) run and the results stay
+ * on the device; *h_width, *h_s (chain length) and *h_h (hull size) tell
+ * the caller how much to allocate, then chp_last_outputs copies them out
+ * (h_Lpairs: width pairs, h_chain: s points, h_hull: h points; any may be
+ * NULL).  The results stay valid until the next host call on the context. */
+int chp_precondition_run(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int want_hull,
+                         int64_t* h_bbox4, int64_t* h_width, int64_t* h_s, int64_t* h_h);
+int chp_last_outputs(chp_ctx* ctx, int32_t* h_Lpairs, int32_t* h_chain, int32_t* h_hull);
 
 /* ------------------------------------------------- synthetic workloads
  * Deterministic, counter-based generators of the BASELINE.json configs

@@ -105,15 +105,17 @@ bool is_pinned(const void* p) {
 }
 
 // Streams h_xy[0..n) to the device in chunks and enqueues launch(d, m) on
-// the compute stream for each chunk as soon as its copy has landed.
+// the compute stream for each chunk as soon as its copy has landed.  With
+// d_dest the chunks land in d_dest[0..2n) (the input stays resident), else
+// in two alternating device staging buffers.
 template <typename Launch>
-int stream_chunks(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, Launch&& launch) {
+int stream_chunks(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, Launch&& launch, int32_t* d_dest = nullptr) {
     if (n == 0) return CHP_OK;
     const bool pinned = is_pinned(h_xy);
     const uint64_t chunk = std::min<uint64_t>(kChunkPts, n);
     const size_t bytes = (size_t)chunk * 8;
     int rc;
-    for (int b = 0; b < 2; ++b)
+    for (int b = 0; b < 2 && !d_dest; ++b)
         if ((rc = chp_ensure(ctx, ctx->stage_dev[b], bytes))) return rc;
     if (!pinned && ctx->stage_bytes < bytes) {
         for (int b = 0; b < 2; ++b) {
@@ -135,17 +137,28 @@ int stream_chunks(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, Launch&& launch
         const int32_t* src = h_xy + 2 * off;
         if (!pinned) {
             // The previous H2D out of this staging buffer must have finished.
+            // The copy into pinned staging runs on the host pool (one thread
+            // copies ~14 GB/s, a quarter of what PCIe drains).
             CHP_CUDA(ctx, cudaEventSynchronize(ctx->ev_copied[b]));
-            std::memcpy(ctx->stage_host[b], src, (size_t)m * 8);
+            char* dst = static_cast<char*>(ctx->stage_host[b]);
+            const char* from = reinterpret_cast<const char*>(src);
+            const size_t total = (size_t)m * 8;
+            HostPool* pool = pool_of(ctx);
+            const int parts = pool->parts();
+            pool->run([&](int i) {
+                const size_t lo = (total * (size_t)i / parts) & ~(size_t)63;
+                const size_t hi = i + 1 == parts ? total : (total * (size_t)(i + 1) / parts) & ~(size_t)63;
+                std::memcpy(dst + lo, from + lo, hi - lo);
+            });
             src = (const int32_t*)ctx->stage_host[b];
         }
+        int32_t* dst = d_dest ? d_dest + 2 * off : (int32_t*)ctx->stage_dev[b].p;
         CHP_CUDA(ctx, cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_consumed[b], 0));
-        CHP_CUDA(ctx, cudaMemcpyAsync(ctx->stage_dev[b].p, src, (size_t)m * 8, cudaMemcpyHostToDevice,
-                                      ctx->copy_stream));
+        CHP_CUDA(ctx, cudaMemcpyAsync(dst, src, (size_t)m * 8, cudaMemcpyHostToDevice, ctx->copy_stream));
         ctx->h2d_bytes += (uint64_t)m * 8;
         CHP_CUDA(ctx, cudaEventRecord(ctx->ev_copied[b], ctx->copy_stream));
         CHP_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_copied[b], 0));
-        if ((rc = launch((const int32_t*)ctx->stage_dev[b].p, m))) return rc;
+        if ((rc = launch((const int32_t*)dst, m))) return rc;
         CHP_CUDA(ctx, cudaEventRecord(ctx->ev_consumed[b], ctx->stream));
     }
     return CHP_OK;
@@ -157,17 +170,17 @@ int stream_chunks(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, Launch&& launch
 // staging is only read by the DMA engine, so skipping the read-for-ownership
 // saves a third of the host memory traffic.
 uint32_t pack16_sse2(const int32_t* __restrict__ src, uint32_t* __restrict__ dst, uint64_t m, uint32_t base,
-                uint32_t wcheck, uint32_t qmax) {
+                     uint32_t ybase, uint32_t wcheck, uint32_t qmax) {
     uint32_t bad = 0;
     uint64_t i = 0;
     auto one = [&](uint64_t k) {
         const uint32_t s = (uint32_t)src[2 * k] - base;
-        const uint32_t ym1 = (uint32_t)src[2 * k + 1] - 1u;
+        const uint32_t ym1 = (uint32_t)src[2 * k + 1] - ybase;
         bad |= (uint32_t)(s >= wcheck) | (uint32_t)(ym1 >= qmax);
         dst[k] = s | (ym1 << 16);
     };
     for (; i < m && (reinterpret_cast<uintptr_t>(dst + i) & 15); ++i) one(i);
-    const __m128i vbase = _mm_set1_epi32((int)base), vone = _mm_set1_epi32(1);
+    const __m128i vbase = _mm_set1_epi32((int)base), vone = _mm_set1_epi32((int)ybase);
     const __m128i sign = _mm_set1_epi32((int)0x80000000u);
     const __m128i wlim = _mm_set1_epi32((int)(wcheck ^ 0x80000000u)), qlim = _mm_set1_epi32((int)(qmax ^ 0x80000000u));
     __m128i okv = _mm_set1_epi32(-1);
@@ -192,16 +205,17 @@ uint32_t pack16_sse2(const int32_t* __restrict__ src, uint32_t* __restrict__ dst
 // Gpts/s for SSE2 on the 16-core GPU host.  Unsigned range checks as
 // max_epu32(v, lim) == v  <=>  v >= lim.
 __attribute__((target("avx2"))) uint32_t pack16_avx2(const int32_t* __restrict__ src, uint32_t* __restrict__ dst,
-                                                     uint64_t m, uint32_t base, uint32_t wcheck, uint32_t qmax) {
+                                                     uint64_t m, uint32_t base, uint32_t ybase, uint32_t wcheck,
+                                                     uint32_t qmax) {
     uint64_t i = 0;
     uint32_t bad = 0;
     for (; i < m && (reinterpret_cast<uintptr_t>(dst + i) & 31); ++i) {
         const uint32_t s = (uint32_t)src[2 * i] - base;
-        const uint32_t ym1 = (uint32_t)src[2 * i + 1] - 1u;
+        const uint32_t ym1 = (uint32_t)src[2 * i + 1] - ybase;
         bad |= (uint32_t)(s >= wcheck) | (uint32_t)(ym1 >= qmax);
         dst[i] = s | (ym1 << 16);
     }
-    const __m256i vbase = _mm256_set1_epi32((int)base), vone = _mm256_set1_epi32(1);
+    const __m256i vbase = _mm256_set1_epi32((int)base), vone = _mm256_set1_epi32((int)ybase);
     const __m256i wl = _mm256_set1_epi32((int)wcheck), ql = _mm256_set1_epi32((int)qmax);
     const __m256i perm = _mm256_setr_epi32(0, 2, 4, 6, 1, 3, 5, 7);
     __m256i badv = _mm256_setzero_si256();
@@ -218,7 +232,7 @@ __attribute__((target("avx2"))) uint32_t pack16_avx2(const int32_t* __restrict__
     }
     for (; i < m; ++i) {
         const uint32_t s = (uint32_t)src[2 * i] - base;
-        const uint32_t ym1 = (uint32_t)src[2 * i + 1] - 1u;
+        const uint32_t ym1 = (uint32_t)src[2 * i + 1] - ybase;
         bad |= (uint32_t)(s >= wcheck) | (uint32_t)(ym1 >= qmax);
         dst[i] = s | (ym1 << 16);
     }
@@ -226,9 +240,11 @@ __attribute__((target("avx2"))) uint32_t pack16_avx2(const int32_t* __restrict__
     return bad | (uint32_t)!_mm256_testz_si256(badv, badv);
 }
 
-uint32_t pack16(const int32_t* src, uint32_t* dst, uint64_t m, uint32_t base, uint32_t wcheck, uint32_t qmax) {
+uint32_t pack16(const int32_t* src, uint32_t* dst, uint64_t m, uint32_t base, uint32_t ybase, uint32_t wcheck,
+                uint32_t qmax) {
     static const bool avx2 = __builtin_cpu_supports("avx2");
-    return avx2 ? pack16_avx2(src, dst, m, base, wcheck, qmax) : pack16_sse2(src, dst, m, base, wcheck, qmax);
+    return avx2 ? pack16_avx2(src, dst, m, base, ybase, wcheck, qmax)
+                : pack16_sse2(src, dst, m, base, ybase, wcheck, qmax);
 }
 
 // Packed form of stream_chunks for width <= 2^16 and 1 <= y <= q <= 2^16:
@@ -244,8 +260,8 @@ uint32_t pack16(const int32_t* src, uint32_t* dst, uint64_t m, uint32_t base, ui
 // DMA'd straight from the END of the input (K1 validates those itself), so
 // the packed front and the raw back meet where both resources finish.
 template <typename Launch>
-int stream_chunks_packed(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t x_off, uint32_t wcheck,
-                         uint32_t qmax, bool* bad, Launch&& launch) {
+int stream_chunks_packed(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t x_off, int32_t ybase,
+                         uint32_t wcheck, uint32_t qmax, bool* bad, Launch&& launch) {
     *bad = false;
     if (n == 0) return CHP_OK;
     // 8 Mi points per chunk (e2e C2, hybrid: 2 Mi 8.7-9.1, 4 Mi 9.4-9.7, 8 Mi
@@ -327,7 +343,7 @@ int stream_chunks_packed(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t 
         pool->run([&](int i) {
             const uint64_t lo = (mm * (uint64_t)i / parts) & ~7ull;
             const uint64_t hi = i + 1 == parts ? mm : (mm * (uint64_t)(i + 1) / parts) & ~7ull;
-            part_bad[(size_t)i] = pack16(src + 2 * lo, dst + lo, hi - lo, base, wcheck, qmax);
+            part_bad[(size_t)i] = pack16(src + 2 * lo, dst + lo, hi - lo, base, (uint32_t)ybase, wcheck, qmax);
         });
         const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         if (mm >= (1u << 20) && dt > 0) ctx->pack_rate = 0.5 * ctx->pack_rate + 0.5 * (double)mm / dt;
@@ -339,7 +355,7 @@ int stream_chunks_packed(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t 
         dma_ahead = (double)mm * 4 / kPcieBps;
         CHP_CUDA(ctx, cudaEventRecord(ctx->ev_copied[b], ctx->copy_stream));
         CHP_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_copied[b], 0));
-        if ((rc = chp_unpack16(ctx, (const uint32_t*)ctx->stage_dev[b].p, mm, (int32_t)base,
+        if ((rc = chp_unpack16(ctx, (const uint32_t*)ctx->stage_dev[b].p, mm, (int32_t)base, ybase,
                                (int32_t*)ctx->unpack_dev[b].p)))
             return rc;
         CHP_CUDA(ctx, cudaEventRecord(ctx->ev_consumed[b], ctx->stream));
@@ -350,22 +366,25 @@ int stream_chunks_packed(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t 
     return CHP_OK;
 }
 
-// Streams h_xy[0..n) into ctx->dl (accumulating; it must be initialised).
-// Inputs whose slots and y values fit 16 bits travel packed (half the PCIe
-// bytes) unless CHP_PIPELINE_NO_PACK is set in flags.
-int stream_reduce(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t width, int64_t q, int64_t x_off,
-                  uint32_t flags) {
+// Streams h_xy[0..n) into ctx->dl (accumulating; it must be initialised),
+// valid y in [ybase, ybase + ycount) (ycount < 0: no upper bound).  Inputs
+// whose slots and y offsets fit 16 bits travel packed (half the PCIe bytes)
+// unless CHP_PIPELINE_NO_PACK is set in flags or the environment.
+int stream_reduce(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t width, int64_t ybase, int64_t ycount,
+                  int64_t x_off, uint32_t flags) {
     auto launch = [&](const int32_t* d, uint64_t m) {
-        return chp_reduce(ctx, d, m, width, q, x_off, (int32_t*)ctx->dl.p, flags | CHP_REDUCE_ACCUMULATE);
+        return chp_reduce_yr(ctx, d, m, width, ybase, ycount, x_off, (int32_t*)ctx->dl.p,
+                             flags | CHP_REDUCE_ACCUMULATE);
     };
-    const bool packable = width <= 65536 && q >= 1 && q <= 65536 && !(flags & CHP_REDUCE_NO_VALIDATE) &&
+    const bool packable = width <= 65536 && ycount >= 1 && ycount <= 65536 && !(flags & CHP_REDUCE_NO_VALIDATE) &&
                           !(flags & CHP_PIPELINE_NO_PACK) && !std::getenv("CHP_PIPELINE_NO_PACK") &&
-                          x_off + 1 >= (int64_t)INT32_MIN &&
-                          x_off <= (int64_t)INT32_MAX;
+                          x_off + 1 >= (int64_t)INT32_MIN && x_off <= (int64_t)INT32_MAX &&
+                          ybase >= (int64_t)INT32_MIN && ybase <= (int64_t)INT32_MAX;
     if (!packable) return stream_chunks(ctx, h_xy, n, launch);
     const uint32_t wcheck = (uint32_t)std::min<int64_t>(width, (int64_t)INT32_MAX - x_off);
+    const uint32_t qmax = (uint32_t)std::min<int64_t>(ycount, (int64_t)INT32_MAX - ybase + 1);
     bool bad = false;
-    int rc = stream_chunks_packed(ctx, h_xy, n, x_off, wcheck, (uint32_t)q, &bad, launch);
+    int rc = stream_chunks_packed(ctx, h_xy, n, x_off, (int32_t)ybase, wcheck, qmax, &bad, launch);
     if (rc) return rc;
     if (bad) {  // same outcome as the unpacked path: the error word of DL
         int32_t minus1 = -1;
@@ -376,17 +395,16 @@ int stream_reduce(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t width, 
     return CHP_OK;
 }
 
-// Compaction (+ hull) of ctx->dl, then the requested outputs to the host.
-int finish_host(chp_ctx* ctx, int64_t width, int64_t major_off, int64_t minor_off, int32_t* h_Lpairs,
-                uint64_t* h_occ, int32_t* h_chain, int64_t* h_s, int32_t* h_hull, int64_t* h_h,
-                bool chain_required) {
+// Compaction (+ hull) of ctx->dl into the context's device buffers; cnt
+// receives the K3/K4 counts {s, v, err, s-v, h}.
+int finish_device(chp_ctx* ctx, int64_t width, int64_t major_off, int64_t minor_off, bool want_chain,
+                  bool want_lpairs, bool want_occ, bool want_hull, int64_t cnt[8]) {
     int rc;
     const size_t W = (size_t)width;
     if ((rc = chp_ensure(ctx, ctx->counts, 16 * sizeof(int64_t)))) return rc;
     if ((rc = chp_ensure(ctx, ctx->chain, 2 * W * 8))) return rc;
     if ((rc = chp_ensure(ctx, ctx->occ, ((W + 63) / 64) * 8))) return rc;
     if ((rc = chp_ensure(ctx, ctx->lpairs, W * 8))) return rc;
-    const bool want_hull = h_hull || h_h;
     if (want_hull) {
         if ((rc = chp_ensure(ctx, ctx->lower, W * 8))) return rc;
         if ((rc = chp_ensure(ctx, ctx->upper, W * 8))) return rc;
@@ -394,8 +412,8 @@ int finish_host(chp_ctx* ctx, int64_t width, int64_t major_off, int64_t minor_of
     }
     int64_t* d_counts = (int64_t*)ctx->counts.p;
     if ((rc = chp_compact(ctx, (const int32_t*)ctx->dl.p, width, major_off, minor_off, 0,
-                          (h_chain || h_s) ? (int32_t*)ctx->chain.p : nullptr,
-                          h_occ ? (uint64_t*)ctx->occ.p : nullptr, h_Lpairs ? (int32_t*)ctx->lpairs.p : nullptr,
+                          want_chain ? (int32_t*)ctx->chain.p : nullptr, want_occ ? (uint64_t*)ctx->occ.p : nullptr,
+                          want_lpairs ? (int32_t*)ctx->lpairs.p : nullptr,
                           want_hull ? (int32_t*)ctx->lower.p : nullptr,
                           want_hull ? (int32_t*)ctx->upper.p : nullptr, nullptr, d_counts)))
         return rc;
@@ -404,27 +422,43 @@ int finish_host(chp_ctx* ctx, int64_t width, int64_t major_off, int64_t minor_of
                            (int32_t*)ctx->hull.p, d_counts + 4)))
             return rc;
     }
-    int64_t cnt[8];
-    CHP_CUDA(ctx, cudaMemcpyAsync(cnt, d_counts, sizeof cnt, cudaMemcpyDeviceToHost, ctx->stream));
+    CHP_CUDA(ctx, cudaMemcpyAsync(cnt, d_counts, 8 * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
     CHP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-    if (cnt[2] != 0) return chp_einval(ctx, "reduce: coordinate out of range");
-    const int64_t s = cnt[0];
-    if (h_s) *h_s = s;
-    if (s == 0 && chain_required) return chp_einval(ctx, "build_polyline: no valid points");
+    if (!want_hull) cnt[4] = 0;
+    return CHP_OK;
+}
+
+// The context's device results to host buffers (any may be NULL).
+int copy_out(chp_ctx* ctx, int64_t width, int64_t s, int64_t h, int32_t* h_Lpairs, uint64_t* h_occ,
+             int32_t* h_chain, int32_t* h_hull) {
+    const size_t W = (size_t)width;
     if (h_Lpairs)
         CHP_CUDA(ctx, cudaMemcpyAsync(h_Lpairs, ctx->lpairs.p, W * 8, cudaMemcpyDeviceToHost, ctx->stream));
     if (h_occ)
         CHP_CUDA(ctx, cudaMemcpyAsync(h_occ, ctx->occ.p, ((W + 63) / 64) * 8, cudaMemcpyDeviceToHost, ctx->stream));
     if (h_chain && s > 0)
         CHP_CUDA(ctx, cudaMemcpyAsync(h_chain, ctx->chain.p, (size_t)s * 8, cudaMemcpyDeviceToHost, ctx->stream));
-    if (want_hull) {
-        if (h_h) *h_h = cnt[4];
-        if (h_hull && cnt[4] > 0)
-            CHP_CUDA(ctx, cudaMemcpyAsync(h_hull, ctx->hull.p, (size_t)cnt[4] * 8, cudaMemcpyDeviceToHost,
-                                          ctx->stream));
-    }
+    if (h_hull && h > 0)
+        CHP_CUDA(ctx, cudaMemcpyAsync(h_hull, ctx->hull.p, (size_t)h * 8, cudaMemcpyDeviceToHost, ctx->stream));
     CHP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     return CHP_OK;
+}
+
+// Compaction (+ hull) of ctx->dl, then the requested outputs to the host.
+int finish_host(chp_ctx* ctx, int64_t width, int64_t major_off, int64_t minor_off, int32_t* h_Lpairs,
+                uint64_t* h_occ, int32_t* h_chain, int64_t* h_s, int32_t* h_hull, int64_t* h_h,
+                bool chain_required) {
+    int64_t cnt[8];
+    const bool want_hull = h_hull || h_h;
+    int rc = finish_device(ctx, width, major_off, minor_off, h_chain || h_s, h_Lpairs != nullptr, h_occ != nullptr,
+                           want_hull, cnt);
+    if (rc) return rc;
+    if (cnt[2] != 0) return chp_einval(ctx, "reduce: coordinate out of range");
+    const int64_t s = cnt[0];
+    if (h_s) *h_s = s;
+    if (s == 0 && chain_required) return chp_einval(ctx, "build_polyline: no valid points");
+    if (want_hull && h_h) *h_h = cnt[4];
+    return copy_out(ctx, width, s, cnt[4], h_Lpairs, h_occ, h_chain, h_hull);
 }
 
 }  // namespace
@@ -469,6 +503,7 @@ void chp_ctx_destroy(chp_ctx* ctx) {
     for (DevBuf* b : bufs) free_buf(*b);
     free_buf(ctx->unpack_dev[0]);
     free_buf(ctx->unpack_dev[1]);
+    free_buf(ctx->points);
     free_buf(ctx->raw_dev[0]);
     free_buf(ctx->raw_dev[1]);
     for (int b = 0; b < 2; ++b) {
@@ -520,13 +555,14 @@ int chp_pipeline_host(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t wid
                       int64_t* h_h) {
     if (!ctx) return CHP_EINVAL;
     ctx->h2d_bytes = 0;
+    ctx->last_valid = false;
     if (width < 1) return chp_einval(ctx, "reduce: width must be >= 1");
     if (width > (1ll << 29)) return chp_einval(ctx, "reduce: width exceeds the device limit 2^29");
     CHP_CUDA(ctx, cudaSetDevice(ctx->device));
     int rc;
     if ((rc = chp_ensure(ctx, ctx->dl, chp_dl_len(width) * 4))) return rc;
     if ((rc = chp_dl_init(ctx, (int32_t*)ctx->dl.p, width))) return rc;
-    if ((rc = stream_reduce(ctx, h_xy, n, width, q, 0, 0))) return rc;
+    if ((rc = stream_reduce(ctx, h_xy, n, width, 1, q, 0, 0))) return rc;
     return finish_host(ctx, width, 0, 0, h_Lpairs, h_occ, h_chain, h_s, h_hull, h_h,
                        h_chain != nullptr || h_hull != nullptr);
 }
@@ -534,6 +570,7 @@ int chp_pipeline_host(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t wid
 int chp_translate_host(chp_ctx* ctx, const int32_t* h_in, uint64_t n, int32_t dx, int32_t dy, int32_t* h_out) {
     if (!ctx) return CHP_EINVAL;
     ctx->h2d_bytes = 0;
+    ctx->last_valid = false;
     if (n == 0) return CHP_OK;
     CHP_CUDA(ctx, cudaSetDevice(ctx->device));
     DevBuf buf;
@@ -555,6 +592,7 @@ int chp_polyline_host(chp_ctx* ctx, const int32_t* h_Lpairs, int64_t width, int6
                       int swapped, int32_t* h_chain, int64_t* h_s) {
     if (!ctx) return CHP_EINVAL;
     ctx->h2d_bytes = 0;
+    ctx->last_valid = false;
     if (width < 1 || width > (1ll << 29)) return chp_einval(ctx, "build_polyline: width must be in [1, 2^29]");
     CHP_CUDA(ctx, cudaSetDevice(ctx->device));
     int rc;
@@ -580,28 +618,34 @@ int chp_polyline_host(chp_ctx* ctx, const int32_t* h_Lpairs, int64_t width, int6
     return CHP_OK;
 }
 
-int chp_precondition_host(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t* h_bbox4, int32_t* h_Lpairs, int32_t* h_chain,
-                          int64_t* h_s, int32_t* h_hull, int64_t* h_h) {
+static int precondition_core(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t* h_bbox4, bool bounds_only,
+                             const std::function<int(int64_t width, int64_t x_off)>& finish) {
     if (!ctx) return CHP_EINVAL;
     ctx->h2d_bytes = 0;
+    ctx->last_valid = false;
     if (n == 0) return chp_einval(ctx, "precondition: empty input");
     CHP_CUDA(ctx, cudaSetDevice(ctx->device));
     // Step 1 (bounds).  The points stay resident for step 3 when they fit a
-    // quarter of free memory; otherwise they are streamed twice.
+    // quarter of free memory (copied in chunks, the bounds of each chunk
+    // computed as it lands; the buffer is kept in the context); otherwise
+    // they are streamed twice.
     int rc;
     size_t freeb = 0, totalb = 0;
     CHP_CUDA(ctx, cudaMemGetInfo(&freeb, &totalb));
-    const bool resident = (size_t)n * 8 <= freeb / 4;
-    DevBuf pts;
-    if (resident) {
-        if ((rc = chp_ensure(ctx, pts, (size_t)n * 8))) return rc;
-        CHP_CUDA(ctx, cudaMemcpyAsync(pts.p, h_xy, (size_t)n * 8, cudaMemcpyHostToDevice, ctx->stream));
-    }
+    // (CHP_PRECONDITION_STREAM forces the streamed form: tests only.)
+    const bool resident = (size_t)n * 8 <= (freeb + ctx->points.bytes) / 4 && !std::getenv("CHP_PRECONDITION_STREAM");
+    DevBuf& pts = ctx->points;
     if ((rc = chp_ensure(ctx, ctx->counts, 16 * sizeof(int64_t)))) return rc;
     int32_t* d_b4 = (int32_t*)((int64_t*)ctx->counts.p + 8);
     int32_t b4[4];
     if (resident) {
-        if ((rc = chp_bounds(ctx, (const int32_t*)pts.p, n, d_b4))) return rc;
+        if ((rc = chp_ensure(ctx, pts, (size_t)n * 8))) return rc;
+        if ((rc = chp_bounds_init(ctx, d_b4))) return rc;
+        if ((rc = stream_chunks(
+                 ctx, h_xy, n,
+                 [&](const int32_t* d, uint64_t m) { return chp_bounds_accumulate(ctx, d, m, d_b4); },
+                 (int32_t*)pts.p)))
+            return rc;
         CHP_CUDA(ctx, cudaMemcpyAsync(b4, d_b4, 16, cudaMemcpyDeviceToHost, ctx->stream));
         CHP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     } else {
@@ -615,31 +659,73 @@ int chp_precondition_host(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t
     }
     for (int i = 0; i < 4; ++i) h_bbox4[i] = b4[i];
     const int64_t width = (int64_t)b4[1] - b4[0] + 1;
-    if (!h_chain && !h_hull && !h_s && !h_Lpairs) {
-        free_buf(pts);
-        return CHP_OK;
-    }
-    if (width > (1ll << 29)) {
-        free_buf(pts);
-        return chp_einval(ctx, "precondition: x extent exceeds the device limit 2^29");
-    }
+    if (bounds_only) return CHP_OK;
+    if (width > (1ll << 29)) return chp_einval(ctx, "precondition: x extent exceeds the device limit 2^29");
     const int64_t x_off = (int64_t)b4[0] - 1;  // major_offset, src/reducer.cpp:258
     if ((rc = chp_ensure(ctx, ctx->dl, chp_dl_len(width) * 4))) return rc;
+    // Every point lies in the bounding box, so K1 runs with the box's y range
+    // as the valid range: the filter variants (and, streamed, the 16-bit
+    // packing) apply, and validation can never fire.
+    // (A y range of 2^32 - 1 or more values does not fit the uint32 test:
+    // then no validation and no y range, as the reference's bucket().)
+    int64_t ybase = b4[2], ycount = (int64_t)b4[3] - b4[2] + 1;
+    uint32_t rflags = 0;
+    if (ycount >= (1ll << 32) - 1) {
+        ybase = 1;
+        ycount = -1;
+        rflags = CHP_REDUCE_NO_VALIDATE;
+    }
     if (resident) {
-        rc = chp_reduce(ctx, (const int32_t*)pts.p, n, width, -1, x_off, (int32_t*)ctx->dl.p,
-                        CHP_REDUCE_NO_VALIDATE);
+        rc = chp_reduce_yr(ctx, (const int32_t*)pts.p, n, width, ybase, ycount, x_off, (int32_t*)ctx->dl.p, rflags);
     } else {
         rc = chp_dl_init(ctx, (int32_t*)ctx->dl.p, width);
-        if (!rc) rc = stream_reduce(ctx, h_xy, n, width, -1, x_off, CHP_REDUCE_NO_VALIDATE);
+        if (!rc) rc = stream_reduce(ctx, h_xy, n, width, ybase, ycount, x_off, rflags);
     }
-    if (rc) {
-        free_buf(pts);
-        return rc;
-    }
-    rc = finish_host(ctx, width, x_off, 0, h_Lpairs, nullptr, h_chain, h_s, h_hull, h_h, true);
-    cudaStreamSynchronize(ctx->stream);
-    free_buf(pts);
-    return rc;
+    if (rc) return rc;
+    return finish(width, x_off);
+}
+
+
+int chp_precondition_host(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t* h_bbox4, int32_t* h_Lpairs,
+                          int32_t* h_chain, int64_t* h_s, int32_t* h_hull, int64_t* h_h) {
+    const bool bounds_only = !h_chain && !h_hull && !h_s && !h_Lpairs && !h_h;
+    return precondition_core(ctx, h_xy, n, h_bbox4, bounds_only, [&](int64_t width, int64_t x_off) {
+        return finish_host(ctx, width, x_off, 0, h_Lpairs, nullptr, h_chain, h_s, h_hull, h_h, true);
+    });
+}
+
+int chp_precondition_run(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int want_hull, int64_t* h_bbox4,
+                         int64_t* h_width, int64_t* h_s, int64_t* h_h) {
+    if (ctx) ctx->last_valid = false;
+    int64_t width = 0, s = 0, h = 0;
+    const int rc = precondition_core(ctx, h_xy, n, h_bbox4, false, [&](int64_t w, int64_t x_off) {
+        int64_t cnt[8];
+        int r = finish_device(ctx, w, x_off, 0, true, true, false, want_hull != 0, cnt);
+        if (r) return r;
+        if (cnt[2] != 0) return chp_einval(ctx, "reduce: coordinate out of range");
+        if (cnt[0] == 0) return chp_einval(ctx, "build_polyline: no valid points");
+        width = w;
+        s = cnt[0];
+        h = cnt[4];
+        return CHP_OK;
+    });
+    if (rc) return rc;
+    ctx->last_valid = true;
+    ctx->last_width = width;
+    ctx->last_s = s;
+    ctx->last_h = want_hull ? h : -1;
+    if (h_width) *h_width = width;
+    if (h_s) *h_s = s;
+    if (h_h) *h_h = want_hull ? h : 0;
+    return CHP_OK;
+}
+
+int chp_last_outputs(chp_ctx* ctx, int32_t* h_Lpairs, int32_t* h_chain, int32_t* h_hull) {
+    if (!ctx) return CHP_EINVAL;
+    if (!ctx->last_valid) return chp_einval(ctx, "last_outputs: no chp_precondition_run result on this context");
+    if (h_hull && ctx->last_h < 0) return chp_einval(ctx, "last_outputs: the run did not compute the hull");
+    return copy_out(ctx, ctx->last_width, ctx->last_s, ctx->last_h < 0 ? 0 : ctx->last_h, h_Lpairs, nullptr, h_chain,
+                    h_hull);
 }
 
 }  // extern "C"

@@ -57,6 +57,10 @@ struct chp_ctx {
     // Hybrid packed pipeline: int32 chunks DMA'd straight from a pinned input
     // while the host packs (abi.cu), and the measured host pack rate.
     DevBuf raw_dev[2];
+    DevBuf points;  // precondition: the resident input (bounds, then K1)
+    // chp_precondition_run's results, held on device until chp_last_outputs
+    bool last_valid = false;
+    int64_t last_width = 0, last_s = 0, last_h = -1;
     cudaEvent_t ev_rcopied[2] = {nullptr, nullptr};
     cudaEvent_t ev_rconsumed[2] = {nullptr, nullptr};
     double pack_rate = 8e9;  // points / s
@@ -107,7 +111,10 @@ int chp_bounds_init(chp_ctx* ctx, int32_t* d_out4);
 int chp_bounds_accumulate(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int32_t* d_out4);
 // Packed host pipeline (abi.cu): 32-bit words (slot | (y - 1) << 16) back to
 // int32 (x, y) pairs with x = slot + base.
-int chp_unpack16(chp_ctx* ctx, const uint32_t* d_in, uint64_t n, int32_t base, int32_t* d_out);
+int chp_unpack16(chp_ctx* ctx, const uint32_t* d_in, uint64_t n, int32_t base, int32_t ybase, int32_t* d_out);
+// K1 with a general valid y range [ybase, ybase + ycount) (reduce.cu).
+int chp_reduce_yr(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t width, int64_t ybase, int64_t ycount,
+                  int64_t x_off, int32_t* d_L, uint32_t flags);
 
 // ----------------------------------------------------------- device side
 

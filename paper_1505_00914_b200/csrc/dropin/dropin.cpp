@@ -115,19 +115,26 @@ occupancy::Index index_from_entries(const std::vector<reducer::ColumnExtremes>& 
 }
 
 // Canonical hull of a point set on the device, along whichever axis keeps
-// the column count within the device limit.
+// the column count within the device limit.  One pass over the input
+// (chp_precondition_run); only an x extent beyond 2^29 costs a second pass
+// along y.
 Hull device_hull(std::span<const Point> pts) {
     if (pts.empty()) throw std::invalid_argument("hull: empty input");
     auto xy = narrow(pts);
-    const BoundingBox bb = bounds_of(xy);
-    const bool swap = bb.width() > (1ll << 29) && bb.height() < bb.width();
-    if (swap) xy = narrow(pts, true);
-    int64_t b4[4];
-    const int64_t w = swap ? bb.height() : bb.width();
-    if (w > (1ll << 29)) throw std::invalid_argument("hull: point extent exceeds the device limit 2^29");
-    std::vector<int32_t> hull(2 * static_cast<size_t>(2 * w + 2));
-    int64_t h = 0;
-    check(chp_precondition_host(ctx(), xy.data(), xy.size() / 2, b4, nullptr, nullptr, nullptr, hull.data(), &h));
+    int64_t b4[4] = {0, 0, 0, 0}, w = 0, s = 0, h = 0;
+    int rc = chp_precondition_run(ctx(), xy.data(), xy.size() / 2, 1, b4, &w, &s, &h);
+    bool swap = false;
+    if (rc == CHP_EINVAL && b4[1] - b4[0] + 1 > (1ll << 29)) {
+        const BoundingBox bb{b4[0], b4[1], b4[2], b4[3]};
+        if (bb.height() > (1ll << 29) || bb.height() >= bb.width())
+            throw std::invalid_argument("hull: point extent exceeds the device limit 2^29");
+        swap = true;
+        xy = narrow(pts, true);
+        rc = chp_precondition_run(ctx(), xy.data(), xy.size() / 2, 1, b4, &w, &s, &h);
+    }
+    check(rc);
+    std::vector<int32_t> hull(2 * static_cast<size_t>(h));
+    check(chp_last_outputs(ctx(), nullptr, nullptr, hull.data()));
     std::vector<Point> v = widen(hull.data(), h, swap);
     if (swap) {
         // A reflection: restore CCW order, start at the lexicographic minimum.
@@ -335,19 +342,27 @@ PreconditionResult precondition(std::span<const Point> points, const Preconditio
     using clock = std::chrono::steady_clock;
     auto t0 = clock::now();
     auto xy = detail::narrow(points);
-    const BoundingBox bb = detail::bounds_of(xy);
     const bool full_bounds = options.second_scan || options.auto_axis;
-    const bool swap = options.auto_axis && bb.height() < bb.width();
-    if (swap) xy = detail::narrow(points, true);
+    // auto_axis needs the box before choosing the axis (one bounds-only pass);
+    // otherwise bounds, fold, compaction are ONE pass (chp_precondition_run).
+    bool swap = false;
+    if (options.auto_axis) {
+        const BoundingBox bb0 = detail::bounds_of(xy);
+        swap = bb0.height() < bb0.width();
+        if (swap) xy = detail::narrow(points, true);
+    }
     auto t1 = clock::now();
-    const std::int64_t width = swap ? bb.height() : bb.width();
-    const std::int64_t major_offset = (swap ? bb.y_min : bb.x_min) - 1;
-    const std::int64_t minor_offset = full_bounds ? (swap ? bb.x_min : bb.y_min) - 1 : 0;
-    if (width > (1ll << 29)) throw std::invalid_argument("precondition: extent exceeds the device limit 2^29");
-    std::vector<int32_t> L(2 * static_cast<size_t>(width)), chain(4 * static_cast<size_t>(width));
-    int64_t b4[4], s = 0;
-    detail::check(chp_precondition_host(detail::ctx(), xy.data(), points.size(), b4, L.data(), chain.data(), &s,
-                                        nullptr, nullptr));
+    int64_t b4[4] = {0, 0, 0, 0}, width = 0, s = 0;
+    const int rc = chp_precondition_run(detail::ctx(), xy.data(), points.size(), 0, b4, &width, &s, nullptr);
+    if (rc == CHP_EINVAL && b4[1] - b4[0] + 1 > (1ll << 29))
+        throw std::invalid_argument("precondition: extent exceeds the device limit 2^29");
+    detail::check(rc);
+    // b4 is the box of the (possibly axis-swapped) input
+    const BoundingBox bb = swap ? BoundingBox{b4[2], b4[3], b4[0], b4[1]} : BoundingBox{b4[0], b4[1], b4[2], b4[3]};
+    const std::int64_t major_offset = b4[0] - 1;
+    const std::int64_t minor_offset = full_bounds ? b4[2] - 1 : 0;
+    std::vector<int32_t> L(2 * static_cast<size_t>(width)), chain(2 * static_cast<size_t>(s));
+    detail::check(chp_last_outputs(detail::ctx(), L.data(), chain.data(), nullptr));
     PreconditionResult res{ExtremalArray{detail::entries_from_pairs(L, minor_offset),
                                          occupancy::Index(1, options.occ_kind)},
                            {}, bb};

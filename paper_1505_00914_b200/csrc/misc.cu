@@ -106,7 +106,7 @@ Clusters make_clusters(uint64_t seed, int64_t p) {
 namespace {
 // Four packed points (one 16-byte load) -> two 16-byte stores.
 __global__ void k_unpack16(const uint4* __restrict__ in4, uint64_t n4, const uint32_t* __restrict__ in, uint64_t n,
-                           int32_t base, int4* __restrict__ out4, int2* __restrict__ out) {
+                           int32_t base, int32_t ybase, int4* __restrict__ out4, int2* __restrict__ out) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
         const uint4 q = __ldcs(in4 + i);
@@ -115,23 +115,23 @@ __global__ void k_unpack16(const uint4* __restrict__ in4, uint64_t n4, const uin
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             v[2 * k] = (int)(w[k] & 0xFFFFu) + base;
-            v[2 * k + 1] = (int)(w[k] >> 16) + 1;
+            v[2 * k + 1] = (int)(w[k] >> 16) + ybase;
         }
         out4[2 * i] = make_int4(v[0], v[1], v[2], v[3]);
         out4[2 * i + 1] = make_int4(v[4], v[5], v[6], v[7]);
     }
     if (blockIdx.x == 0)
         for (uint64_t i = 4 * n4 + threadIdx.x; i < n; i += blockDim.x)
-            out[i] = make_int2((int)(in[i] & 0xFFFFu) + base, (int)(in[i] >> 16) + 1);
+            out[i] = make_int2((int)(in[i] & 0xFFFFu) + base, (int)(in[i] >> 16) + ybase);
 }
 }  // namespace
 
-int chp_unpack16(chp_ctx* ctx, const uint32_t* d_in, uint64_t n, int32_t base, int32_t* d_out) {
+int chp_unpack16(chp_ctx* ctx, const uint32_t* d_in, uint64_t n, int32_t base, int32_t ybase, int32_t* d_out) {
     if (n == 0) return CHP_OK;
     const bool vec = !(reinterpret_cast<uintptr_t>(d_in) & 15) && !(reinterpret_cast<uintptr_t>(d_out) & 15);
     const uint64_t n4 = vec ? n / 4 : 0;
     const int blocks = (int)std::min<uint64_t>((n4 + 255) / 256 + 1, (uint64_t)ctx->sm_count * 8);
-    k_unpack16<<<blocks, 256, 0, ctx->stream>>>(reinterpret_cast<const uint4*>(d_in), n4, d_in, n, base,
+    k_unpack16<<<blocks, 256, 0, ctx->stream>>>(reinterpret_cast<const uint4*>(d_in), n4, d_in, n, base, ybase,
                                                 reinterpret_cast<int4*>(d_out), reinterpret_cast<int2*>(d_out));
     CHP_LAUNCHED(ctx);
     return CHP_OK;

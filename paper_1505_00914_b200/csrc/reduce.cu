@@ -45,7 +45,8 @@ constexpr int kThreads = 1024;
 struct Geo {
     uint32_t base;    // x_off + 1 (mod 2^32): slot = x - base
     uint32_t wcheck;  // slots reachable by an int32 x: min(width, INT_MAX - x_off)
-    uint32_t qmax;    // valid y: (uint32)(y - 1) < qmax  (VALIDATE only)
+    uint32_t ybase;   // lowest valid y (1 for reduce; the bbox minimum for precondition)
+    uint32_t qmax;    // valid y: (uint32)(y - ybase) < qmax  (VALIDATE only)
 };
 
 // Split the (possibly only 8-byte aligned) point array into an optional
@@ -68,7 +69,7 @@ template <bool VALIDATE>
 __device__ __forceinline__ bool accept(const Geo& g, int32_t x, int32_t y, uint32_t& s) {
     s = slot_of(x, g.base);
     bool ok = s < g.wcheck;
-    if (VALIDATE) ok = ok && ((uint32_t)y - 1u < g.qmax);
+    if (VALIDATE) ok = ok && ((uint32_t)y - g.ybase < g.qmax);
     return ok;
 }
 
@@ -350,11 +351,11 @@ __global__ void __launch_bounds__(kThreads) k_reduce_smem16(const int32_t* __res
     // the shared window base (S2UR + ULEA) and the Geo words (LDCU) are
     // rematerialised for every point.
     const uint32_t tbase = pin((uint32_t)__cvta_generic_to_shared(smem4));
-    const uint32_t base = pin(g.base), wcheck = pin(g.wcheck), qmax = pin(g.qmax);
+    const uint32_t base = pin(g.base), wcheck = pin(g.wcheck), qmax = pin(g.qmax), ybase = pin(g.ybase);
     uint32_t bad = 0;
     auto one = [&](int32_t x, int32_t y) {
         uint32_t s = slot_of(x, base);
-        const uint32_t ym1 = (uint32_t)y - 1u;
+        const uint32_t ym1 = (uint32_t)y - ybase;
         const bool ok = (s < wcheck) & (ym1 < qmax);
         bad |= !ok;
         s = ok ? s : 0u;
@@ -378,8 +379,8 @@ __global__ void __launch_bounds__(kThreads) k_reduce_smem16(const int32_t* __res
         const uint32_t w = sW[c];
         const uint32_t a = w & 0xFFFFu, b = w >> 16;
         if (a > 0xFFFFu - b) continue;  // lo > hi: empty
-        const int32_t lo = 1 + (int32_t)a;
-        const int32_t nhi = ~(1 + (int32_t)(0xFFFFu - b));
+        const int32_t lo = (int32_t)(g.ybase + a);
+        const int32_t nhi = ~(int32_t)(g.ybase + (0xFFFFu - b));
         const int2 cur = ld_cg2(gL + c);
         if (lo < cur.x) red_min(DL + 2ull * c, lo);
         if (nhi < cur.y) red_min(DL + 2ull * c + 1, nhi);
@@ -458,7 +459,8 @@ __device__ __forceinline__ uint32_t lds_w(uint32_t addr) {
 // `ngroups` (the sink) and a partial last group are "never".
 template <typename W>
 __global__ void __launch_bounds__(256) k_filter_build(const int* __restrict__ DL, uint32_t width, uint32_t gshift,
-                                                      uint32_t ys, W* __restrict__ F, uint32_t ngroups) {
+                                                      int32_t ybase, uint32_t ys, W* __restrict__ F,
+                                                      uint32_t ngroups) {
     const uint32_t gi = blockIdx.x * blockDim.x + threadIdx.x;
     if (gi > ngroups) return;
     const uint32_t c0 = gi << gshift;
@@ -498,9 +500,10 @@ __global__ void __launch_bounds__(256) k_filter_build(const int* __restrict__ DL
         if (!empty) {
             constexpr long long M = FW<W>::kMask;
             const long long q = 1ll << ys;
-            const long long a = (long long)maxlo - 1;
+            const long long a = (long long)maxlo - ybase;
             const long long fa = a <= 0 ? 0 : (a + q - 1) / q;
-            long long fb = minhi >= 0 ? (long long)minhi / q - 1 : -1;
+            const long long b = (long long)minhi - ybase + 1;
+            long long fb = b >= 0 ? b / q - 1 : -1;
             if (fb > M) fb = M;
             if (fa <= fb) {
                 const long long span = (fb - fa + 1) < M ? (fb - fa + 1) : M;
@@ -544,10 +547,10 @@ __global__ void __launch_bounds__(kThreads) k_reduce_filter(const int32_t* __res
     auto test = [&](int32_t x, int32_t y, uint32_t& s, uint32_t& w) -> bool {
         s = min(slot_of(x, g.base), width);
         w = lds_w<W>(tbase + (s >> gshift) * (uint32_t)sizeof(W));
-        return (((uint32_t)y - 1u) >> ys) - (w & HM) >= (w >> H);
+        return (((uint32_t)y - g.ybase) >> ys) - (w & HM) >= (w >> H);
     };
     auto valid = [&](uint32_t s, int32_t y) {
-        const bool ok = (s < g.wcheck) & ((uint32_t)y - 1u < g.qmax);
+        const bool ok = (s < g.wcheck) & ((uint32_t)y - g.ybase < g.qmax);
         bad |= !ok;
         return ok;
     };
@@ -556,7 +559,7 @@ __global__ void __launch_bounds__(kThreads) k_reduce_filter(const int32_t* __res
     // y >= max_lo, so only hi can move.
     auto settle_red = [&](uint32_t s, int32_t y, uint32_t w) {
         if (!valid(s, y)) return;
-        const uint32_t u = ((uint32_t)y - 1u) >> ys;
+        const uint32_t u = ((uint32_t)y - g.ybase) >> ys;
         const uint32_t fa = w & HM, span = w >> H;
         if (span == 0 || u > fa) red_min(DL + 2ull * s + 1, ~y);  // not known below min_hi
         if (span == 0 || u < fa) red_min(DL + 2ull * s, y);       // not known above max_lo
@@ -645,7 +648,7 @@ __device__ __forceinline__ void sample_fold(const int32_t* __restrict__ xy, uint
                                             uint32_t width, uint32_t ys, uint16_t* T, uint8_t* ring, int stages) {
     auto f = [&](int32_t x, int32_t y) {
         const uint32_t s = min(slot_of(x, g.base), width);
-        const uint32_t u = ((uint32_t)y - 1u) >> ys;
+        const uint32_t u = ((uint32_t)y - g.ybase) >> ys;
         const uint32_t w = T[s];
         const uint32_t nw = min(w & 0xFFu, u) | (max(w >> 8, u) << 8);
         if (nw != w) T[s] = (uint16_t)nw;
@@ -801,7 +804,7 @@ __device__ __forceinline__ void sampled_pass(const int32_t* __restrict__ xy, uin
     // (an out-of-line __noinline__ version measured 411 vs 491 Gpts/s).
     // Validation lives here too: an invalid point always reaches it (below).
     auto settle = [&](uint32_t s, int32_t y) {
-        const uint32_t ym1 = (uint32_t)y - 1u;
+        const uint32_t ym1 = (uint32_t)y - g.ybase;
         if (s >= g.wcheck || ym1 >= g.qmax) {
             bad = 1;
             return;
@@ -833,7 +836,7 @@ __device__ __forceinline__ void sampled_pass(const int32_t* __restrict__ xy, uin
         s = min(slot_of(x, g.base), width);
         const uint32_t w = lds_u16(tbase + 2 * s);
         const uint32_t lo = w & 0xFFu, span = w >> 8;
-        return (((uint32_t)y - 1u) >> ys) - lo >= span;  // not strictly inside
+        return (((uint32_t)y - g.ybase) >> ys) - lo >= span;  // not strictly inside
     };
     auto one = [&](int32_t x, int32_t y) {
         uint32_t s;
@@ -1030,7 +1033,7 @@ __global__ void __launch_bounds__(kThreads) k_reduce_filter8(const int32_t* __re
         }
         const uint32_t f = sF8[s];
         const uint32_t qa = f & 0xFFu, qb = f >> 8;
-        const uint32_t u = ((uint32_t)y - 1u) >> ys;
+        const uint32_t u = ((uint32_t)y - g.ybase) >> ys;
         if (u >= qa && u <= qb) return;
         if (qa > qb) {  // nothing known: both extremes may move
             red_min(DL + 2ull * s, y);
@@ -1169,8 +1172,8 @@ int run_group_filter(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, const Geo& g
     const uint64_t warm = n < (1ull << 22) ? n : (n >> kw) & ~1ull;
     if ((rc = pass(d_xy, warm, nullptr))) return rc;
     for (uint64_t done = warm; done < n;) {
-        k_filter_build<W><<<(ngroups + 1 + 255) / 256, 256, 0, ctx->stream>>>(d_L, w, gshift, ys,
-                                                                            (W*)ctx->filter.p, ngroups);
+        k_filter_build<W><<<(ngroups + 1 + 255) / 256, 256, 0, ctx->stream>>>(d_L, w, gshift, (int32_t)g.ybase,
+                                                                            ys, (W*)ctx->filter.p, ngroups);
         CHP_LAUNCHED(ctx);
         const uint64_t stop = std::min<uint64_t>(n, 2 * done);
         cur_done = done;
@@ -1199,9 +1202,14 @@ extern "C" int chp_dl_init(chp_ctx* ctx, int32_t* d_L, int64_t width) {
 // Choice of variant: the smallest shared-memory
 // footprint that holds the exact table (smem16, then smem32), else the
 // column-group filter when the y range is known, else the L2 table.
-extern "C" int chp_reduce(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t width, int64_t q,
-                          int64_t x_off, int32_t* d_L, uint32_t flags) {
+// Algorithm 1 with the valid y range [ybase, ybase + ycount) (ycount < 0:
+// [ybase, INT32_MAX]).  chp_reduce is ybase = 1, ycount = q; precondition
+// passes the bounding box's y range, so the fast variants apply to it too.
+int chp_reduce_yr(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t width, int64_t ybase, int64_t ycount,
+                  int64_t x_off, int32_t* d_L, uint32_t flags) {
     if (!ctx) return CHP_EINVAL;
+    if (ybase < (int64_t)INT32_MIN || ybase > (int64_t)INT32_MAX) return chp_einval(ctx, "reduce: y base outside int32");
+    const int64_t q = ycount;  // number of valid y values (the variants' bucket range)
     if (width < 1) return chp_einval(ctx, "reduce: width must be >= 1");
     if (width > (int64_t)INT32_MAX) return chp_einval(ctx, "reduce: width exceeds the int32 slot range");
     if ((reinterpret_cast<uintptr_t>(d_xy) & 7) || (reinterpret_cast<uintptr_t>(d_L) & 7))
@@ -1216,13 +1224,16 @@ extern "C" int chp_reduce(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t
     g.base = (uint32_t)(int32_t)(x_off + 1);
     const int64_t reach = (int64_t)INT32_MAX - x_off;  // x <= INT32_MAX
     g.wcheck = (uint32_t)std::min<int64_t>(width, reach);
-    g.qmax = q < 0 ? (uint32_t)INT32_MAX : (uint32_t)std::min<int64_t>(q, INT32_MAX);
+    g.ybase = (uint32_t)(int32_t)ybase;
+    // number of valid y values; the host callers keep it below 2^32
+    g.qmax = (uint32_t)std::min<int64_t>({q < 0 ? (int64_t)INT32_MAX - ybase + 1 : q, (int64_t)INT32_MAX - ybase + 1,
+                                          (int64_t)UINT32_MAX});
     const uint32_t w = (uint32_t)width;
     const size_t budget = (size_t)std::min(ctx->smem_optin, 200 * 1024);
     const bool fits32 = (size_t)w * 8 <= budget;
-    const bool y16 = validate && q >= 1 && q <= 65536;  // all valid y in [1, 65536]
+    const bool y16 = validate && q >= 1 && q <= 65536;  // all valid y in [ybase, ybase + 65536)
     const bool fits16 = y16 && (size_t)w * 4 <= budget;
-    const bool yknown = validate && q >= 1;  // every accepted y is in [1, q]
+    const bool yknown = validate && q >= 1;  // every accepted y is in [ybase, ybase + q)
     const bool fits_f8 = yknown && (size_t)((w + 7) & ~7u) * 2 <= budget;
 
     const uint32_t wpad8 = (w + 8) & ~7u;  // >= w + 1: slot w is the invalid-x sink
@@ -1380,6 +1391,11 @@ extern "C" int chp_reduce(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t
             return CHP_OK;
         }
     }
+}
+
+extern "C" int chp_reduce(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t width, int64_t q,
+                          int64_t x_off, int32_t* d_L, uint32_t flags) {
+    return chp_reduce_yr(ctx, d_xy, n, width, 1, q, x_off, d_L, flags);
 }
 
 extern "C" int chp_check(chp_ctx* ctx, const int32_t* d_L, int64_t width) {

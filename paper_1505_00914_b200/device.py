@@ -254,26 +254,29 @@ class Context:
         return ch[: int(s[0])]
 
     def precondition_host(self, xy: np.ndarray, chain: bool = True, hull: bool = False) -> dict:
+        """chp::reducer::precondition from a host buffer in one pass over the
+        input (chp_precondition_run), outputs fetched once the width is known."""
         xy = np.ascontiguousarray(xy, dtype=np.int32)
         n = xy.size // 2
         bbox = np.zeros(4, np.int64)
-        # Bounds first (learns the width), then the sized outputs.
-        self._check(self.L.chp_precondition_host(self.h, _np_ptr(xy), n, _np_ptr(bbox), None, None, None, None,
-                                                 None))
         if not chain and not hull:
+            self._check(self.L.chp_precondition_host(self.h, _np_ptr(xy), n, _np_ptr(bbox), None, None, None, None,
+                                                     None))
             return {"bbox": tuple(int(v) for v in bbox)}
-        w = int(bbox[1] - bbox[0] + 1)
-        Lp = np.empty((w, 2), np.int32)
-        ch = np.empty((2 * w, 2), np.int32)
-        hl = np.empty((2 * w + 2, 2), np.int32) if hull else None
+        w = np.zeros(1, np.int64)
         s = np.zeros(1, np.int64)
         h = np.zeros(1, np.int64)
-        self._check(self.L.chp_precondition_host(self.h, _np_ptr(xy), n, _np_ptr(bbox), _np_ptr(Lp), _np_ptr(ch),
-                                                 _np_ptr(s), _np_ptr(hl), _np_ptr(h) if hull else None))
+        self._check(self.L.chp_precondition_run(self.h, _np_ptr(xy), n, int(bool(hull)), _np_ptr(bbox), _np_ptr(w),
+                                                _np_ptr(s), _np_ptr(h)))
+        w, s, h = int(w[0]), int(s[0]), int(h[0])
+        Lp = np.empty((w, 2), np.int32)
+        ch = np.empty((s, 2), np.int32)
+        hl = np.empty((max(h, 1), 2), np.int32) if hull else None
+        self._check(self.L.chp_last_outputs(self.h, _np_ptr(Lp), _np_ptr(ch), _np_ptr(hl) if hull else None))
         out = {"bbox": tuple(int(v) for v in bbox), "width": w, "major_offset": int(bbox[0]) - 1,
-               "L": Lp, "chain": ch[: int(s[0])], "s": int(s[0])}
+               "L": Lp, "chain": ch, "s": s}
         if hull:
-            out["hull"] = hl[: int(h[0])]
+            out["hull"] = hl[:h]
         return out
 
 

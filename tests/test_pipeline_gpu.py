@@ -109,3 +109,58 @@ def test_pipeline_host_packed_extremes(ctx, orc):
     ref = orc.pipeline(xy, p, p)
     assert np.array_equal(out["L"], ref["L"])
     assert np.array_equal(out["chain"], ref["chain"])
+
+
+# precondition runs K1 with the bounding box's y range as the valid range
+# (ybase = ymin), so the filter variants and the 16-bit packing apply to
+# untranslated inputs; a range of 2^32 - 1 values or more falls back.
+@pytest.mark.parametrize("shift", [(-100_000, -50_000), (7, 1_000_000), (-2**31 + 5, -2**31 + 9)])
+def test_precondition_host_y_range(ctx, orc, shift):
+    xy = generate_host(2, 21, 65536, 2_000_000)
+    xy[:, 0] += shift[0]
+    xy[:, 1] += shift[1]
+    out = ctx.precondition_host(xy, chain=True, hull=True)
+    ref = orc.precondition(xy)
+    assert out["bbox"] == ref["bbox"]
+    assert np.array_equal(out["chain"], ref["chain"])
+    assert np.array_equal(out["hull"], ref["hull"])
+
+
+@pytest.mark.parametrize("ys", [(-2**31, 2**31 - 1), (-2**31 + 1, 2**31 - 1), (-2**31 + 1, 2**31 - 2), (0, 0)])
+def test_precondition_host_extreme_y(ctx, orc, ys):
+    xy = generate_host(3, 5, 1024, 300_000)
+    xy[0, 1] = ys[0]
+    xy[1, 1] = ys[1]
+    out = ctx.precondition_host(xy, chain=True)
+    ref = orc.precondition(xy)
+    assert out["bbox"] == ref["bbox"]
+    assert np.array_equal(out["chain"], ref["chain"])
+
+
+def test_precondition_device_narrow_y_uses_fast_variant(ctx, orc):
+    # y range of 300 values at a negative offset: smem16 with ybase != 1
+    rng = np.random.default_rng(3)
+    xy = np.stack([rng.integers(-5000, -4000, 1_000_000), rng.integers(-70_000, -69_700, 1_000_000)], 1)
+    xy = xy.astype(np.int32)
+    out = ctx.precondition_host(xy, chain=True, hull=True)
+    assert ctx.variant in ("smem16", "smem16+tma")
+    ref = orc.precondition(xy)
+    assert out["bbox"] == ref["bbox"]
+    assert np.array_equal(out["chain"], ref["chain"])
+    assert np.array_equal(out["hull"], ref["hull"])
+
+
+@pytest.mark.parametrize("shift", [(0, 0), (-100_000, -50_000), (3, 2**31 - 70_000)])
+def test_precondition_host_streamed(ctx, orc, shift, monkeypatch):
+    # the form taken when the input does not fit a quarter of free device
+    # memory: bounds streamed, then K1 streamed (packed when the box fits 16 bits)
+    monkeypatch.setenv("CHP_PRECONDITION_STREAM", "1")
+    xy = generate_host(2, 22, 65536, 20_000_001)
+    xy[:, 0] += shift[0]
+    xy[:, 1] += shift[1]
+    out = ctx.precondition_host(xy, chain=True, hull=True)
+    assert ctx.last_h2d_bytes == 8 * len(xy) + 4 * len(xy)  # int32 bounds pass + packed K1 pass
+    ref = orc.precondition(xy)
+    assert out["bbox"] == ref["bbox"]
+    assert np.array_equal(out["chain"], ref["chain"])
+    assert np.array_equal(out["hull"], ref["hull"])
