@@ -261,7 +261,7 @@ uint32_t pack16(const int32_t* src, uint32_t* dst, uint64_t m, uint32_t base, ui
 // the packed front and the raw back meet where both resources finish.
 template <typename Launch>
 int stream_chunks_packed(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t x_off, int32_t ybase,
-                         uint32_t wcheck, uint32_t qmax, bool* bad, Launch&& launch) {
+                         uint32_t wcheck, uint32_t qmax, bool speculative, bool* bad, Launch&& launch) {
     *bad = false;
     if (n == 0) return CHP_OK;
     // 8 Mi points per chunk (e2e C2, hybrid: 2 Mi 8.7-9.1, 4 Mi 9.4-9.7, 8 Mi
@@ -269,13 +269,14 @@ int stream_chunks_packed(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t 
     constexpr uint64_t kPackChunk = 8ull << 20;
     constexpr double kPcieBps = 50e9;  // H2D bytes / s (PCIe 5 x16, measured ~55e9)
     const uint64_t chunk = std::min<uint64_t>(kPackChunk, n);
-    const bool hybrid = is_pinned(h_xy);
+    const bool pinned = is_pinned(h_xy);
+    const bool hybrid = pinned;
     int rc;
     for (int b = 0; b < 2; ++b) {
         if ((rc = chp_ensure(ctx, ctx->stage_dev[b], (size_t)chunk * 4))) return rc;
         if ((rc = chp_ensure(ctx, ctx->unpack_dev[b], (size_t)chunk * 8))) return rc;
-        if (hybrid && (rc = chp_ensure(ctx, ctx->raw_dev[b], (size_t)chunk * 8))) return rc;
-        if (hybrid && !ctx->ev_rcopied[b]) {
+        if ((hybrid || speculative) && (rc = chp_ensure(ctx, ctx->raw_dev[b], (size_t)chunk * 8))) return rc;
+        if ((hybrid || speculative) && !ctx->ev_rcopied[b]) {
             CHP_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_rcopied[b], cudaEventDisableTiming));
             CHP_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_rconsumed[b], cudaEventDisableTiming));
         }
@@ -290,10 +291,18 @@ int stream_chunks_packed(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t 
     }
     HostPool* pool = pool_of(ctx);
     const uint32_t base = (uint32_t)(int32_t)(x_off + 1);
+    if (speculative && !pinned && ctx->stage_bytes < (size_t)chunk * 8) {
+        for (int b = 0; b < 2; ++b) {
+            if (ctx->stage_host[b]) cudaFreeHost(ctx->stage_host[b]);
+            ctx->stage_host[b] = nullptr;
+        }
+        for (int b = 0; b < 2; ++b) CHP_CUDA(ctx, cudaMallocHost(&ctx->stage_host[b], (size_t)chunk * 8));
+        ctx->stage_bytes = (size_t)chunk * 8;
+    }
     for (int b = 0; b < 2; ++b) {
         CHP_CUDA(ctx, cudaEventRecord(ctx->ev_consumed[b], ctx->stream));
         CHP_CUDA(ctx, cudaEventRecord(ctx->ev_copied[b], ctx->copy_stream));
-        if (hybrid) {
+        if (hybrid || speculative) {
             CHP_CUDA(ctx, cudaEventRecord(ctx->ev_rconsumed[b], ctx->stream));
             CHP_CUDA(ctx, cudaEventRecord(ctx->ev_rcopied[b], ctx->copy_stream));
         }
@@ -323,6 +332,34 @@ int stream_chunks_packed(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t 
         }
         return CHP_OK;
     };
+    // One int32 chunk [off, off+m) to the device and through K1 (which
+    // validates it): a speculatively packed chunk that did not fit 16 bits.
+    auto send_raw = [&](uint64_t off, uint64_t m) -> int {
+        const int rb = (int)(kr++ & 1);
+        const int32_t* src = h_xy + 2 * off;
+        if (!pinned) {
+            CHP_CUDA(ctx, cudaEventSynchronize(ctx->ev_rcopied[rb]));
+            char* dst = static_cast<char*>(ctx->stage_host[rb]);
+            const char* from = reinterpret_cast<const char*>(src);
+            const size_t total = (size_t)m * 8;
+            const int parts = pool->parts();
+            pool->run([&](int i) {
+                const size_t lo = (total * (size_t)i / parts) & ~(size_t)63;
+                const size_t hi = i + 1 == parts ? total : (total * (size_t)(i + 1) / parts) & ~(size_t)63;
+                std::memcpy(dst + lo, from + lo, hi - lo);
+            });
+            src = static_cast<const int32_t*>(ctx->stage_host[rb]);
+        }
+        CHP_CUDA(ctx, cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_rconsumed[rb], 0));
+        CHP_CUDA(ctx, cudaMemcpyAsync(ctx->raw_dev[rb].p, src, (size_t)m * 8, cudaMemcpyHostToDevice, ctx->copy_stream));
+        ctx->h2d_bytes += (uint64_t)m * 8;
+        CHP_CUDA(ctx, cudaEventRecord(ctx->ev_rcopied[rb], ctx->copy_stream));
+        CHP_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_rcopied[rb], 0));
+        int r = launch((const int32_t*)ctx->raw_dev[rb].p, m);
+        if (r) return r;
+        CHP_CUDA(ctx, cudaEventRecord(ctx->ev_rconsumed[rb], ctx->stream));
+        return CHP_OK;
+    };
     double dma_ahead = 0;  // copy-engine seconds already queued when a pack starts
     while (front < back) {
         const uint64_t m = std::min<uint64_t>(chunk, back - front);
@@ -347,7 +384,15 @@ int stream_chunks_packed(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t 
         });
         const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         if (mm >= (1u << 20) && dt > 0) ctx->pack_rate = 0.5 * ctx->pack_rate + 0.5 * (double)mm / dt;
-        for (uint32_t v : part_bad) any_bad |= v;
+        uint32_t chunk_bad = 0;
+        for (uint32_t v : part_bad) chunk_bad |= v;
+        if (chunk_bad && speculative) {  // not 16-bit: the chunk goes as int32 pairs
+            if ((rc = send_raw(front, mm))) return rc;
+            front += mm;
+            dma_ahead = (double)mm * 8 / kPcieBps;
+            continue;
+        }
+        any_bad |= chunk_bad;
         CHP_CUDA(ctx, cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_consumed[b], 0));
         CHP_CUDA(ctx, cudaMemcpyAsync(ctx->stage_dev[b].p, dst, (size_t)mm * 4, cudaMemcpyHostToDevice,
                                       ctx->copy_stream));
@@ -376,15 +421,20 @@ int stream_reduce(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t width, 
         return chp_reduce_yr(ctx, d, m, width, ybase, ycount, x_off, (int32_t*)ctx->dl.p,
                              flags | CHP_REDUCE_ACCUMULATE);
     };
-    const bool packable = width <= 65536 && ycount >= 1 && ycount <= 65536 && !(flags & CHP_REDUCE_NO_VALIDATE) &&
+    // ycount < 0 (no upper bound, the reference's default q = nullopt):
+    // pack speculatively against a 2^16 window; chunks with a larger y go
+    // as int32 pairs and K1 validates them.
+    const bool speculative = ycount < 0;
+    const bool packable = width <= 65536 && (speculative || ycount <= 65536) && ycount != 0 &&
+                          !(flags & CHP_REDUCE_NO_VALIDATE) &&
                           !(flags & CHP_PIPELINE_NO_PACK) && !std::getenv("CHP_PIPELINE_NO_PACK") &&
                           x_off + 1 >= (int64_t)INT32_MIN && x_off <= (int64_t)INT32_MAX &&
                           ybase >= (int64_t)INT32_MIN && ybase <= (int64_t)INT32_MAX;
     if (!packable) return stream_chunks(ctx, h_xy, n, launch);
     const uint32_t wcheck = (uint32_t)std::min<int64_t>(width, (int64_t)INT32_MAX - x_off);
-    const uint32_t qmax = (uint32_t)std::min<int64_t>(ycount, (int64_t)INT32_MAX - ybase + 1);
+    const uint32_t qmax = (uint32_t)std::min<int64_t>(speculative ? 65536 : ycount, (int64_t)INT32_MAX - ybase + 1);
     bool bad = false;
-    int rc = stream_chunks_packed(ctx, h_xy, n, x_off, (int32_t)ybase, wcheck, qmax, &bad, launch);
+    int rc = stream_chunks_packed(ctx, h_xy, n, x_off, (int32_t)ybase, wcheck, qmax, speculative, &bad, launch);
     if (rc) return rc;
     if (bad) {  // same outcome as the unpacked path: the error word of DL
         int32_t minus1 = -1;

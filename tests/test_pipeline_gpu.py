@@ -164,3 +164,38 @@ def test_precondition_host_streamed(ctx, orc, shift, monkeypatch):
     assert out["bbox"] == ref["bbox"]
     assert np.array_equal(out["chain"], ref["chain"])
     assert np.array_equal(out["hull"], ref["hull"])
+
+
+# q unset (the reference's default, y only >= 1): the host packs
+# speculatively against a 2^16 window; a chunk holding a larger y goes as
+# int32 pairs, and K1 validates it.
+@pytest.mark.parametrize("pinned", [False, True])
+@pytest.mark.parametrize("big_y_at", [None, 5, 9_000_000, 17_999_999])
+def test_pipeline_host_q_unset(ctx, orc, pinned, big_y_at):
+    p = 65536
+    xy = generate_host(2, 31, p, 18_000_000)
+    if big_y_at is not None:
+        xy[big_y_at, 1] = 2**31 - 1  # valid without q
+    if pinned:
+        xy = _pinned(xy)
+    out = ctx.pipeline_host(xy, p, None, L=True, chain=True)
+    assert 4 * len(xy) <= ctx.last_h2d_bytes <= 8 * len(xy)
+    if not pinned:  # pageable: packed, except the one 8 Mi-point chunk holding the big y
+        c = 8 << 20
+        extra = 0 if big_y_at is None else 4 * min(c, len(xy) - (big_y_at // c) * c)
+        assert ctx.last_h2d_bytes == 4 * len(xy) + extra
+    ref = orc.pipeline(xy, p, None)
+    assert np.array_equal(out["L"], ref["L"])
+    assert np.array_equal(out["chain"], ref["chain"])
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+@pytest.mark.parametrize("bad", [(7, 0), (0, 7), (65537, 7), (7, -5)])
+def test_pipeline_host_q_unset_invalid(ctx, pinned, bad):
+    p = 65536
+    xy = generate_host(2, 32, p, 3_000_000)
+    xy[2_500_000] = bad
+    if pinned:
+        xy = _pinned(xy)
+    with pytest.raises(ValueError):
+        ctx.pipeline_host(xy, p, None)
