@@ -1234,7 +1234,7 @@ int chp_reduce_yr(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t width, 
     const bool y16 = validate && q >= 1 && q <= 65536;  // all valid y in [ybase, ybase + 65536)
     const bool fits16 = y16 && (size_t)w * 4 <= budget;
     const bool yknown = validate && q >= 1;  // every accepted y is in [ybase, ybase + q)
-    const bool fits_f8 = yknown && (size_t)((w + 7) & ~7u) * 2 <= budget;
+    const bool fits_f8 = yknown && ybase == 1 && (size_t)((w + 7) & ~7u) * 2 <= budget;  // quant8 assumes y >= 1
 
     const uint32_t wpad8 = (w + 8) & ~7u;  // >= w + 1: slot w is the invalid-x sink
     const bool fits_sampled = yknown && g.wcheck == w && (size_t)wpad8 * 2 <= budget;
