@@ -20,6 +20,8 @@ REDUCE_FORCE_FILTER = 16
 REDUCE_FORCE_FILTER8 = 32
 REDUCE_FORCE_SMEM16 = 64
 REDUCE_FORCE_SAMPLED = 8192
+REDUCE_FUSED = 16384
+REDUCE_SAMPLE_SPLIT = 1 << 25
 
 _lib = None
 

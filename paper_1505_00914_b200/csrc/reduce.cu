@@ -929,9 +929,11 @@ __device__ __noinline__ void sampled_main_pass(const int32_t* __restrict__ xy, u
 __global__ void __launch_bounds__(kThreads) k_sampled_fused(const int32_t* __restrict__ xy, uint64_t n, uint64_t ns,
                                                             Geo g, uint32_t width, uint32_t wpad, uint32_t ys,
                                                             uint16_t* __restrict__ scratch, uint16_t* __restrict__ F,
-                                                            int* __restrict__ DL, int init_dl, GridBar* bar) {
+                                                            int* __restrict__ DL, int init_dl, GridBar* bar,
+                                                            int merge_only) {
     extern __shared__ uint4 smem4[];
     const uint32_t nchunks = wpad / 8;
+    if (merge_only) pdl_trigger();  // the main pass (a dependent launch) may queue
     // ---- A: sample pass + DL init
     sample_init(smem4, wpad, DL, width, init_dl);
     __syncthreads();
@@ -971,6 +973,7 @@ __global__ void __launch_bounds__(kThreads) k_sampled_fused(const int32_t* __res
             __syncthreads();
         }
     }
+    if (merge_only) return;  // the main pass is a separate (dependent) launch
     grid_barrier(bar);
     // ---- C: every CTA loads the merged table
     {
@@ -1326,10 +1329,15 @@ int chp_reduce_yr(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t width, 
             // (C2: k=3 510.7, k=4 505.2, k=5 474.4, k=6 430.0 Gpts/s).
             const uint32_t kshift = (flags >> 16) & 7 ? (flags >> 16) & 7 : 3;
             const uint64_t ns = std::min<uint64_t>(n, std::max<uint64_t>(n >> kshift, 2)) & ~1ull;
-            if ((flags & CHP_REDUCE_FUSED) && !(flags & CHP_REDUCE_TMA) && ctx->coop) {
-                // One cooperative kernel (grid barriers between the phases).
-                // Opt-in: measured 433-486 vs 495 Gpts/s for three launches
-                // (its main pass spills at 64 registers).
+            // Default: sample pass + merge as ONE cooperative kernel (a grid
+            // barrier between them, the merge spread over every CTA), then the
+            // main pass as a dependent launch (C2: 586 vs 573 Gpts/s for
+            // separate sample / merge launches, CHP_REDUCE_SAMPLE_SPLIT).
+            // CHP_REDUCE_FUSED also runs the main pass inside the same kernel
+            // (slower: its main pass spills at 64 registers).
+            const int merge_only = (flags & CHP_REDUCE_FUSED) ? 0 : 1;
+            if (!(flags & CHP_REDUCE_SAMPLE_SPLIT) && !(flags & CHP_REDUCE_TMA) &&
+                !(flags & CHP_REDUCE_SAMPLE_TMA) && ctx->coop) {
                 if (!ctx->gridbar.p) {
                     if ((rc = chp_ensure(ctx, ctx->gridbar, 64))) return rc;
                     CHP_CUDA(ctx, cudaMemsetAsync(ctx->gridbar.p, 0, 64, ctx->stream));
@@ -1345,11 +1353,19 @@ int chp_reduce_yr(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t width, 
                     uint16_t* F = (uint16_t*)ctx->filter.p;
                     GridBar* bar = (GridBar*)ctx->gridbar.p;
                     void* args[] = {(void*)&d_xy, (void*)&n,     (void*)&ns, (void*)&g,   (void*)&w,   (void*)&wpad8,
-                                    (void*)&ys,   (void*)&scratch, (void*)&F, (void*)&d_L, (void*)&init, (void*)&bar};
+                                    (void*)&ys,   (void*)&scratch, (void*)&F, (void*)&d_L, (void*)&init, (void*)&bar,
+                                    (void*)&merge_only};
                     CHP_CUDA(ctx, cudaLaunchCooperativeKernel((const void*)k_sampled_fused, dim3(sblocks),
                                                               dim3(kThreads), args, smem, ctx->stream));
                     CHP_LAUNCHED(ctx);
-                    ctx->variant = "sampled-fused";
+                    if (!merge_only) {
+                        ctx->variant = "sampled-fused";
+                        return CHP_OK;
+                    }
+                    const Plan pl = plan_for(ctx, tbytes, flags, false);
+                    CHP_LAUNCH_PLANNED_PDL(ctx, pl, k_reduce_sampled<true>, k_reduce_sampled<false>, d_xy, n, g, w,
+                                           wpad8, ys, (const uint16_t*)ctx->filter.p, pl.stages, d_L);
+                    ctx->variant = "sampled";
                     return CHP_OK;
                 }
             }

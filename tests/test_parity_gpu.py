@@ -33,6 +33,7 @@ VARIANTS = {
     "filter_red": _lib.REDUCE_FORCE_FILTER | 128,
     "filter_read_tma": _lib.REDUCE_FORCE_FILTER | 256 | 4096,
     "sampled_tma": _lib.REDUCE_FORCE_SAMPLED | 4096,
+    "sampled_split": _lib.REDUCE_FORCE_SAMPLED | _lib.REDUCE_SAMPLE_SPLIT,
 }
 
 
