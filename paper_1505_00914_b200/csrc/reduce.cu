@@ -1355,8 +1355,15 @@ int chp_reduce_yr(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t width, 
                     void* args[] = {(void*)&d_xy, (void*)&n,     (void*)&ns, (void*)&g,   (void*)&w,   (void*)&wpad8,
                                     (void*)&ys,   (void*)&scratch, (void*)&F, (void*)&d_L, (void*)&init, (void*)&bar,
                                     (void*)&merge_only};
-                    CHP_CUDA(ctx, cudaLaunchCooperativeKernel((const void*)k_sampled_fused, dim3(sblocks),
-                                                              dim3(kThreads), args, smem, ctx->stream));
+                    // (A cooperative launch can be refused when the GPU is
+                    // shared and the grid cannot be co-resident: then the
+                    // split form below runs instead.)
+                    const cudaError_t ce = cudaLaunchCooperativeKernel((const void*)k_sampled_fused, dim3(sblocks),
+                                                                       dim3(kThreads), args, smem, ctx->stream);
+                    if (ce != cudaSuccess) {
+                        cudaGetLastError();
+                        goto split;
+                    }
                     CHP_LAUNCHED(ctx);
                     if (!merge_only) {
                         ctx->variant = "sampled-fused";
@@ -1369,6 +1376,7 @@ int chp_reduce_yr(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t width, 
                     return CHP_OK;
                 }
             }
+        split:
             {
                 const Plan sp = plan_for(ctx, tbytes, (flags & CHP_REDUCE_SAMPLE_TMA) ? CHP_REDUCE_TMA : 0u, false);
                 auto fn = sp.tma ? k_sample_learn<true> : k_sample_learn<false>;
