@@ -325,6 +325,7 @@ def main():
 
     # End to end through the C ABI from pinned host memory.
     e2e = None
+    precondition_e2e = None
     if not args.no_e2e:
         import numpy as np
 
@@ -357,6 +358,26 @@ def main():
                           "DMA'd from the input's end while the host packs, " if h2d < n * 8 else
                           "16 Mi-point int32 chunks, ")
                        + "H2D overlapped with K1)"}
+        # The reference's main entry, reducer::precondition (bounds unknown:
+        # one pass computes them, then fold and compaction), through the same
+        # pinned buffer: SURVEY 8(f) row 1, reported beside the headline.
+        if world == 1:
+            hn = host.numpy()
+            ctx.precondition_host(hn, chain=True)  # warm-up
+            pts = []
+            for _ in range(args.e2e_steps):
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                ctx.precondition_host(hn, chain=True)
+                b.record(stream)
+                torch.cuda.synchronize()
+                pts.append(a.elapsed_time(b))
+            pre_ms = statistics.median(pts)
+            precondition_e2e = {"value": n / (pre_ms * 1e-3) / 1e9, "unit": "Gpoints/s", "ms_per_step": pre_ms,
+                                "h2d_bytes_per_step": ctx.last_h2d_bytes,
+                                "path": "chp_precondition_run + chp_last_outputs (pinned int32 input, bounds "
+                                        "unknown: one pass with the bounds folded as the chunks land)"}
         del host
 
     base = None
@@ -383,6 +404,7 @@ def main():
             "clocks": clk,
             "hull_ms": min(hs), "hull_vertices": hull_h,
             "e2e": e2e,
+            "precondition_e2e": precondition_e2e,
             "cpu_baseline": base,
         }
         print(json.dumps(line), flush=True)
