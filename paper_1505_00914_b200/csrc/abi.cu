@@ -261,7 +261,8 @@ uint32_t pack16(const int32_t* src, uint32_t* dst, uint64_t m, uint32_t base, ui
 // the packed front and the raw back meet where both resources finish.
 template <typename Launch>
 int stream_chunks_packed(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t x_off, int32_t ybase,
-                         uint32_t wcheck, uint32_t qmax, bool speculative, bool* bad, Launch&& launch) {
+                         uint32_t wcheck, uint32_t qmax, bool speculative, bool* bad, Launch&& launch,
+                         int32_t* d_dest = nullptr) {
     *bad = false;
     if (n == 0) return CHP_OK;
     // 8 Mi points per chunk (e2e C2, hybrid: 2 Mi 8.7-9.1, 4 Mi 9.4-9.7, 8 Mi
@@ -319,12 +320,13 @@ int stream_chunks_packed(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t 
             const uint64_t m = std::min<uint64_t>({want, chunk, back - front});
             const uint64_t off = back - m;
             CHP_CUDA(ctx, cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_rconsumed[rb], 0));
-            CHP_CUDA(ctx, cudaMemcpyAsync(ctx->raw_dev[rb].p, h_xy + 2 * off, (size_t)m * 8, cudaMemcpyHostToDevice,
+            int32_t* rdst = d_dest ? d_dest + 2 * off : (int32_t*)ctx->raw_dev[rb].p;
+            CHP_CUDA(ctx, cudaMemcpyAsync(rdst, h_xy + 2 * off, (size_t)m * 8, cudaMemcpyHostToDevice,
                                           ctx->copy_stream));
             ctx->h2d_bytes += (uint64_t)m * 8;
             CHP_CUDA(ctx, cudaEventRecord(ctx->ev_rcopied[rb], ctx->copy_stream));
             CHP_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_rcopied[rb], 0));
-            int r = launch((const int32_t*)ctx->raw_dev[rb].p, m);
+            int r = launch((const int32_t*)rdst, m);
             if (r) return r;
             CHP_CUDA(ctx, cudaEventRecord(ctx->ev_rconsumed[rb], ctx->stream));
             back = off;
@@ -351,11 +353,12 @@ int stream_chunks_packed(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t 
             src = static_cast<const int32_t*>(ctx->stage_host[rb]);
         }
         CHP_CUDA(ctx, cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_rconsumed[rb], 0));
-        CHP_CUDA(ctx, cudaMemcpyAsync(ctx->raw_dev[rb].p, src, (size_t)m * 8, cudaMemcpyHostToDevice, ctx->copy_stream));
+        int32_t* rdst = d_dest ? d_dest + 2 * off : (int32_t*)ctx->raw_dev[rb].p;
+        CHP_CUDA(ctx, cudaMemcpyAsync(rdst, src, (size_t)m * 8, cudaMemcpyHostToDevice, ctx->copy_stream));
         ctx->h2d_bytes += (uint64_t)m * 8;
         CHP_CUDA(ctx, cudaEventRecord(ctx->ev_rcopied[rb], ctx->copy_stream));
         CHP_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_rcopied[rb], 0));
-        int r = launch((const int32_t*)ctx->raw_dev[rb].p, m);
+        int r = launch((const int32_t*)rdst, m);
         if (r) return r;
         CHP_CUDA(ctx, cudaEventRecord(ctx->ev_rconsumed[rb], ctx->stream));
         return CHP_OK;
@@ -401,14 +404,54 @@ int stream_chunks_packed(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t 
         CHP_CUDA(ctx, cudaEventRecord(ctx->ev_copied[b], ctx->copy_stream));
         CHP_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_copied[b], 0));
         if ((rc = chp_unpack16(ctx, (const uint32_t*)ctx->stage_dev[b].p, mm, (int32_t)base, ybase,
-                               (int32_t*)ctx->unpack_dev[b].p)))
+                               d_dest ? d_dest + 2 * front : (int32_t*)ctx->unpack_dev[b].p)))
             return rc;
         CHP_CUDA(ctx, cudaEventRecord(ctx->ev_consumed[b], ctx->stream));
-        if ((rc = launch((const int32_t*)ctx->unpack_dev[b].p, mm))) return rc;
+        if ((rc = launch(d_dest ? (const int32_t*)(d_dest + 2 * front) : (const int32_t*)ctx->unpack_dev[b].p, mm)))
+            return rc;
         front += mm;
     }
     *bad = any_bad != 0;
     return CHP_OK;
+}
+
+// A 2^16 x 2^16 packing window from the box of the first min(n, 1 Mi)
+// points (host pool), centred in the slack; false when that prefix is
+// already wider or taller than 2^16.
+bool pack_window(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t* wx, int64_t* wy) {
+    const uint64_t m = std::min<uint64_t>(n, 1ull << 20);
+    HostPool* pool = pool_of(ctx);
+    const int parts = pool->parts();
+    std::vector<int32_t> part((size_t)parts * 4);
+    pool->run([&](int i) {
+        int32_t b[4] = {INT32_MAX, INT32_MIN, INT32_MAX, INT32_MIN};
+        const uint64_t lo = m * (uint64_t)i / parts, hi = m * (uint64_t)(i + 1) / parts;
+        for (uint64_t k = lo; k < hi; ++k) {
+            const int32_t x = h_xy[2 * k], y = h_xy[2 * k + 1];
+            b[0] = std::min(b[0], x);
+            b[1] = std::max(b[1], x);
+            b[2] = std::min(b[2], y);
+            b[3] = std::max(b[3], y);
+        }
+        std::memcpy(&part[(size_t)i * 4], b, sizeof b);
+    });
+    int64_t b[4] = {INT32_MAX, INT32_MIN, INT32_MAX, INT32_MIN};
+    for (int i = 0; i < parts; ++i) {
+        b[0] = std::min<int64_t>(b[0], part[(size_t)i * 4]);
+        b[1] = std::max<int64_t>(b[1], part[(size_t)i * 4 + 1]);
+        b[2] = std::min<int64_t>(b[2], part[(size_t)i * 4 + 2]);
+        b[3] = std::max<int64_t>(b[3], part[(size_t)i * 4 + 3]);
+    }
+    auto place = [](int64_t lo, int64_t hi, int64_t* base) {
+        const int64_t ext = hi - lo + 1;
+        if (ext > 65536) return false;
+        int64_t s = lo - (65536 - ext) / 2;
+        s = std::max<int64_t>(s, INT32_MIN);
+        s = std::min<int64_t>(s, (int64_t)INT32_MAX - 65535);
+        *base = s;
+        return true;
+    };
+    return place(b[0], b[1], wx) && place(b[2], b[3], wy);
 }
 
 // Streams h_xy[0..n) into ctx->dl (accumulating; it must be initialised),
@@ -691,11 +734,22 @@ static int precondition_core(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int6
     if (resident) {
         if ((rc = chp_ensure(ctx, pts, (size_t)n * 8))) return rc;
         if ((rc = chp_bounds_init(ctx, d_b4))) return rc;
-        if ((rc = stream_chunks(
-                 ctx, h_xy, n,
-                 [&](const int32_t* d, uint64_t m) { return chp_bounds_accumulate(ctx, d, m, d_b4); },
-                 (int32_t*)pts.p)))
+        auto fold = [&](const int32_t* d, uint64_t m) { return chp_bounds_accumulate(ctx, d, m, d_b4); };
+        // The box is unknown until every point has been seen, so the 16-bit
+        // packing is speculative: a window sized from the first 1 Mi points'
+        // box (centred in the 2^16 slack) packs every chunk that fits, the
+        // rest travel as int32 pairs; either way they land unpacked in the
+        // resident buffer.
+        int64_t wx = 0, wy = 0;
+        const bool win = !std::getenv("CHP_PIPELINE_NO_PACK") && pack_window(ctx, h_xy, n, &wx, &wy);
+        if (win) {
+            bool unused = false;
+            if ((rc = stream_chunks_packed(ctx, h_xy, n, wx - 1, (int32_t)wy, 65536u, 65536u, true, &unused, fold,
+                                           (int32_t*)pts.p)))
+                return rc;
+        } else if ((rc = stream_chunks(ctx, h_xy, n, fold, (int32_t*)pts.p))) {
             return rc;
+        }
         CHP_CUDA(ctx, cudaMemcpyAsync(b4, d_b4, 16, cudaMemcpyDeviceToHost, ctx->stream));
         CHP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     } else {

@@ -199,3 +199,24 @@ def test_pipeline_host_q_unset_invalid(ctx, pinned, bad):
         xy = _pinned(xy)
     with pytest.raises(ValueError):
         ctx.pipeline_host(xy, p, None)
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_precondition_speculative_window(ctx, orc, pinned):
+    # The packing window comes from the first 1 Mi points; later chunks that
+    # leave it (here: x and y spread 4x wider after 9 M points) go as int32.
+    rng = np.random.default_rng(77)
+    n = 20_000_000
+    xy = np.empty((n, 2), np.int32)
+    xy[:9_000_000, 0] = rng.integers(-70_000, -50_000, 9_000_000)
+    xy[:9_000_000, 1] = rng.integers(1000, 30_000, 9_000_000)
+    xy[9_000_000:, 0] = rng.integers(-120_000, 10_000, n - 9_000_000)
+    xy[9_000_000:, 1] = rng.integers(-50_000, 90_000, n - 9_000_000)
+    if pinned:
+        xy = _pinned(xy)
+    out = ctx.precondition_host(xy, chain=True, hull=True)
+    assert 4 * n < ctx.last_h2d_bytes <= 8 * n  # some chunks packed, some not
+    ref = orc.precondition(xy)
+    assert out["bbox"] == ref["bbox"]
+    assert np.array_equal(out["chain"], ref["chain"])
+    assert np.array_equal(out["hull"], ref["hull"])
