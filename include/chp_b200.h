@@ -204,6 +204,18 @@ int chp_precondition_run(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int want
                          int64_t* h_bbox4, int64_t* h_width, int64_t* h_s, int64_t* h_h);
 int chp_last_outputs(chp_ctx* ctx, int32_t* h_Lpairs, int32_t* h_chain, int32_t* h_hull);
 
+/* int64 forms for callers holding the reference's Point {int64 x, y}
+ * (the C++ drop-in): the host pool narrows or packs straight from the int64
+ * pairs (a coordinate outside int32 is CHP_EINVAL), no int32 copy first.
+ * chp_precondition_run64 with swap_axes reads (y, x).  chp_bounds_host64 is
+ * kernels::min_max: K0 on the device over the narrowed points. */
+int chp_pipeline_host64(chp_ctx* ctx, const int64_t* h_xy, uint64_t n, int64_t width, int64_t q,
+                        int32_t* h_Lpairs, uint64_t* h_occ, int32_t* h_chain, int64_t* h_s,
+                        int32_t* h_hull, int64_t* h_h);
+int chp_precondition_run64(chp_ctx* ctx, const int64_t* h_xy, uint64_t n, int swap_axes, int want_hull,
+                           int64_t* h_bbox4, int64_t* h_width, int64_t* h_s, int64_t* h_h);
+int chp_bounds_host64(chp_ctx* ctx, const int64_t* h_xy, uint64_t n, int64_t* h_bbox4);
+
 /* ------------------------------------------------- synthetic workloads
  * Deterministic, counter-based generators of the BASELINE.json configs
  * (DESIGN.md "Workloads"); identical bytes on host and device.  config:

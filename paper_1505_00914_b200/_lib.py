@@ -67,6 +67,9 @@ def load() -> ctypes.CDLL:
         "chp_precondition_host": (c_int, [vp, vp, c_uint64, vp, vp, vp, vp, vp, vp]),
         "chp_precondition_run": (c_int, [vp, vp, c_uint64, c_int, vp, vp, vp, vp]),
         "chp_last_outputs": (c_int, [vp, vp, vp, vp]),
+        "chp_pipeline_host64": (c_int, [vp, vp, c_uint64, c_int64, c_int64, vp, vp, vp, vp, vp, vp]),
+        "chp_precondition_run64": (c_int, [vp, vp, c_uint64, c_int, c_int, vp, vp, vp, vp]),
+        "chp_bounds_host64": (c_int, [vp, vp, c_uint64, vp]),
         "chp_generate": (c_int, [vp, c_int, c_uint64, c_int64, c_uint64, c_uint64, vp]),
         "chp_generate_host": (c_int, [c_int, c_uint64, c_int64, c_uint64, c_uint64, vp, c_int]),
     }
@@ -83,5 +86,6 @@ ABI_SYMBOLS = (
     "chp_ctx_create", "chp_ctx_destroy", "chp_last_error", "chp_ctx_set_stream", "chp_ctx_use_own_stream", "chp_ctx_stream",
     "chp_ctx_sync", "chp_launch_count", "chp_last_variant", "chp_last_h2d_bytes", "chp_dl_len", "chp_reduce", "chp_dl_init",
     "chp_check", "chp_dl_from_pairs", "chp_polyline_host", "chp_compact", "chp_ns_chain", "chp_hull", "chp_bounds", "chp_translate", "chp_translate_host",
-    "chp_pipeline_host", "chp_precondition_host", "chp_precondition_run", "chp_last_outputs", "chp_generate", "chp_generate_host",
+    "chp_pipeline_host", "chp_precondition_host", "chp_precondition_run", "chp_last_outputs", "chp_pipeline_host64", "chp_precondition_run64",
+    "chp_bounds_host64", "chp_generate", "chp_generate_host",
 )

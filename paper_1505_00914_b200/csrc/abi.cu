@@ -37,10 +37,23 @@ class HostPool {
         for (auto& t : th_) t.join();
     }
     int parts() const { return (int)th_.size() + 1; }
-    void run(const std::function<void(int)>& f) {
+    // Parts worth waking for m items (>= 32 Ki each): small host calls stay
+    // on the caller's thread instead of paying 15 wake-ups and their jitter.
+    int parts_for(uint64_t m) const {
+        const uint64_t k = (m + (32u << 10) - 1) / (32u << 10);
+        return (int)std::max<uint64_t>(1, std::min<uint64_t>(k, (uint64_t)parts()));
+    }
+    // f(i) for i in [0, k) (k = parts() by default).
+    void run(const std::function<void(int)>& f, int k = 0) {
+        if (k <= 0 || k > parts()) k = parts();
+        if (k == 1) {
+            f(0);
+            return;
+        }
         {
             std::lock_guard<std::mutex> g(m_);
             job_ = &f;
+            active_ = k;
             pending_ = (int)th_.size();
             ++gen_;
         }
@@ -62,8 +75,9 @@ class HostPool {
                 if (stop_) return;
                 seen = gen_;
                 job = job_;
+                if (id >= active_) job = nullptr;
             }
-            (*job)(id);
+            if (job) (*job)(id);
             {
                 std::lock_guard<std::mutex> g(m_);
                 if (--pending_ == 0) done_.notify_one();
@@ -75,7 +89,7 @@ class HostPool {
     std::condition_variable cv_, done_;
     const std::function<void(int)>* job_ = nullptr;
     uint64_t gen_ = 0;
-    int pending_ = 0;
+    int pending_ = 0, active_ = 0;
     bool stop_ = false;
 };
 
@@ -104,14 +118,54 @@ bool is_pinned(const void* p) {
     return a.type == cudaMemoryTypeHost;
 }
 
+// A host point array: int32 pairs (the C ABI) or int64 pairs (the
+// reference's Point, read directly by the C++ drop-in, optionally with the
+// axes swapped).  Only an int32 array can be DMA'd as is.
+struct HostPts {
+    const int32_t* p32 = nullptr;
+    const int64_t* p64 = nullptr;
+    bool swap = false;  // p64 only: read (y, x)
+    int64_t x(uint64_t i) const { return p64 ? p64[2 * i + (swap ? 1 : 0)] : p32[2 * i]; }
+    int64_t y(uint64_t i) const { return p64 ? p64[2 * i + (swap ? 0 : 1)] : p32[2 * i + 1]; }
+    bool pinned32() const { return p32 && is_pinned(p32); }
+};
+
+// Points [off, off+m) into int32 pairs at dst (pinned staging) on the host
+// pool: a copy for int32 input, a checked narrowing for int64 input.
+// Returns nonzero if a coordinate does not fit int32.
+uint32_t stage_copy(chp_ctx* ctx, const HostPts& in, uint64_t off, uint64_t m, int32_t* dst) {
+    HostPool* pool = pool_of(ctx);
+    const int parts = pool->parts_for(m);
+    std::vector<uint32_t> bad((size_t)parts, 0u);
+    pool->run([&](int i) {
+        const uint64_t lo = m * (uint64_t)i / parts, hi = m * (uint64_t)(i + 1) / parts;
+        if (in.p32) {
+            std::memcpy(dst + 2 * lo, in.p32 + 2 * (off + lo), (size_t)(hi - lo) * 8);
+            return;
+        }
+        uint32_t b = 0;
+        for (uint64_t k = lo; k < hi; ++k) {
+            const int64_t x = in.x(off + k), y = in.y(off + k);
+            b |= (uint32_t)(x != (int32_t)x) | (uint32_t)(y != (int32_t)y);
+            dst[2 * k] = (int32_t)x;
+            dst[2 * k + 1] = (int32_t)y;
+        }
+        bad[(size_t)i] = b;
+    }, parts);
+    uint32_t any = 0;
+    for (uint32_t b : bad) any |= b;
+    return any;
+}
+
 // Streams h_xy[0..n) to the device in chunks and enqueues launch(d, m) on
 // the compute stream for each chunk as soon as its copy has landed.  With
 // d_dest the chunks land in d_dest[0..2n) (the input stays resident), else
 // in two alternating device staging buffers.
 template <typename Launch>
-int stream_chunks(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, Launch&& launch, int32_t* d_dest = nullptr) {
+int stream_chunks(chp_ctx* ctx, const HostPts& in, uint64_t n, Launch&& launch, int32_t* d_dest = nullptr,
+                  uint32_t* narrow_bad = nullptr) {
     if (n == 0) return CHP_OK;
-    const bool pinned = is_pinned(h_xy);
+    const bool pinned = in.pinned32();
     const uint64_t chunk = std::min<uint64_t>(kChunkPts, n);
     const size_t bytes = (size_t)chunk * 8;
     int rc;
@@ -134,22 +188,15 @@ int stream_chunks(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, Launch&& launch
     for (uint64_t off = 0; off < n; off += chunk, ++k) {
         const int b = (int)(k & 1);
         const uint64_t m = std::min<uint64_t>(chunk, n - off);
-        const int32_t* src = h_xy + 2 * off;
+        const int32_t* src = in.p32 ? in.p32 + 2 * off : nullptr;
         if (!pinned) {
             // The previous H2D out of this staging buffer must have finished.
-            // The copy into pinned staging runs on the host pool (one thread
-            // copies ~14 GB/s, a quarter of what PCIe drains).
+            // The copy (or int64 narrowing) into pinned staging runs on the
+            // host pool (one thread copies ~14 GB/s, a quarter of what PCIe
+            // drains).
             CHP_CUDA(ctx, cudaEventSynchronize(ctx->ev_copied[b]));
-            char* dst = static_cast<char*>(ctx->stage_host[b]);
-            const char* from = reinterpret_cast<const char*>(src);
-            const size_t total = (size_t)m * 8;
-            HostPool* pool = pool_of(ctx);
-            const int parts = pool->parts();
-            pool->run([&](int i) {
-                const size_t lo = (total * (size_t)i / parts) & ~(size_t)63;
-                const size_t hi = i + 1 == parts ? total : (total * (size_t)(i + 1) / parts) & ~(size_t)63;
-                std::memcpy(dst + lo, from + lo, hi - lo);
-            });
+            const uint32_t nb = stage_copy(ctx, in, off, m, static_cast<int32_t*>(ctx->stage_host[b]));
+            if (narrow_bad) *narrow_bad |= nb;
             src = (const int32_t*)ctx->stage_host[b];
         }
         int32_t* dst = d_dest ? d_dest + 2 * off : (int32_t*)ctx->stage_dev[b].p;
@@ -247,6 +294,22 @@ uint32_t pack16(const int32_t* src, uint32_t* dst, uint64_t m, uint32_t base, ui
                 : pack16_sse2(src, dst, m, base, ybase, wcheck, qmax);
 }
 
+// pack16 for any host array: the SIMD forms for int32 input, a scalar loop
+// with 64-bit range checks for int64 input (anything outside the window,
+// including a value beyond int32, is flagged).
+uint32_t pack_any(const HostPts& in, uint64_t off, uint64_t m, uint32_t* __restrict__ dst, uint32_t base,
+                  uint32_t ybase, uint32_t wcheck, uint32_t qmax) {
+    if (in.p32) return pack16(in.p32 + 2 * off, dst, m, base, ybase, wcheck, qmax);
+    const int64_t b64 = (int32_t)base, y64 = (int32_t)ybase;
+    uint32_t bad = 0;
+    for (uint64_t k = 0; k < m; ++k) {
+        const int64_t s = in.x(off + k) - b64, t = in.y(off + k) - y64;
+        bad |= (uint32_t)((uint64_t)s >= wcheck) | (uint32_t)((uint64_t)t >= qmax);
+        dst[k] = (uint32_t)s | ((uint32_t)t << 16);
+    }
+    return bad;
+}
+
 // Packed form of stream_chunks for width <= 2^16 and 1 <= y <= q <= 2^16:
 // host workers pack chunk k into pinned 4-byte/point staging while the DMA
 // of chunk k-1 is in flight, so PCIe carries half the bytes; on the device
@@ -260,7 +323,7 @@ uint32_t pack16(const int32_t* src, uint32_t* dst, uint64_t m, uint32_t base, ui
 // DMA'd straight from the END of the input (K1 validates those itself), so
 // the packed front and the raw back meet where both resources finish.
 template <typename Launch>
-int stream_chunks_packed(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t x_off, int32_t ybase,
+int stream_chunks_packed(chp_ctx* ctx, const HostPts& in, uint64_t n, int64_t x_off, int32_t ybase,
                          uint32_t wcheck, uint32_t qmax, bool speculative, bool* bad, Launch&& launch,
                          int32_t* d_dest = nullptr) {
     *bad = false;
@@ -270,7 +333,7 @@ int stream_chunks_packed(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t 
     constexpr uint64_t kPackChunk = 8ull << 20;
     constexpr double kPcieBps = 50e9;  // H2D bytes / s (PCIe 5 x16, measured ~55e9)
     const uint64_t chunk = std::min<uint64_t>(kPackChunk, n);
-    const bool pinned = is_pinned(h_xy);
+    const bool pinned = in.pinned32();
     const bool hybrid = pinned;
     int rc;
     for (int b = 0; b < 2; ++b) {
@@ -308,7 +371,7 @@ int stream_chunks_packed(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t 
             CHP_CUDA(ctx, cudaEventRecord(ctx->ev_rcopied[b], ctx->copy_stream));
         }
     }
-    uint32_t any_bad = 0;
+    uint32_t any_bad = 0, narrow_bad = 0;
     std::vector<uint32_t> part_bad((size_t)pool->parts());
     uint64_t front = 0, back = n;  // packed: [0, front); raw: [back, n)
     uint64_t k = 0, kr = 0;
@@ -321,7 +384,7 @@ int stream_chunks_packed(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t 
             const uint64_t off = back - m;
             CHP_CUDA(ctx, cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_rconsumed[rb], 0));
             int32_t* rdst = d_dest ? d_dest + 2 * off : (int32_t*)ctx->raw_dev[rb].p;
-            CHP_CUDA(ctx, cudaMemcpyAsync(rdst, h_xy + 2 * off, (size_t)m * 8, cudaMemcpyHostToDevice,
+            CHP_CUDA(ctx, cudaMemcpyAsync(rdst, in.p32 + 2 * off, (size_t)m * 8, cudaMemcpyHostToDevice,
                                           ctx->copy_stream));
             ctx->h2d_bytes += (uint64_t)m * 8;
             CHP_CUDA(ctx, cudaEventRecord(ctx->ev_rcopied[rb], ctx->copy_stream));
@@ -338,18 +401,10 @@ int stream_chunks_packed(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t 
     // validates it): a speculatively packed chunk that did not fit 16 bits.
     auto send_raw = [&](uint64_t off, uint64_t m) -> int {
         const int rb = (int)(kr++ & 1);
-        const int32_t* src = h_xy + 2 * off;
+        const int32_t* src = in.p32 ? in.p32 + 2 * off : nullptr;
         if (!pinned) {
             CHP_CUDA(ctx, cudaEventSynchronize(ctx->ev_rcopied[rb]));
-            char* dst = static_cast<char*>(ctx->stage_host[rb]);
-            const char* from = reinterpret_cast<const char*>(src);
-            const size_t total = (size_t)m * 8;
-            const int parts = pool->parts();
-            pool->run([&](int i) {
-                const size_t lo = (total * (size_t)i / parts) & ~(size_t)63;
-                const size_t hi = i + 1 == parts ? total : (total * (size_t)(i + 1) / parts) & ~(size_t)63;
-                std::memcpy(dst + lo, from + lo, hi - lo);
-            });
+            narrow_bad |= stage_copy(ctx, in, off, m, static_cast<int32_t*>(ctx->stage_host[rb]));
             src = static_cast<const int32_t*>(ctx->stage_host[rb]);
         }
         CHP_CUDA(ctx, cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_rconsumed[rb], 0));
@@ -377,14 +432,16 @@ int stream_chunks_packed(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t 
         // The DMA out of this staging buffer (two packed chunks ago) must be done.
         CHP_CUDA(ctx, cudaEventSynchronize(ctx->ev_copied[b]));
         uint32_t* dst = static_cast<uint32_t*>(ctx->pack_host[b]);
-        const int32_t* src = h_xy + 2 * front;
-        const int parts = pool->parts();
+        const int parts = pool->parts_for(mm);
         const auto t0 = std::chrono::steady_clock::now();
-        pool->run([&](int i) {
-            const uint64_t lo = (mm * (uint64_t)i / parts) & ~7ull;
-            const uint64_t hi = i + 1 == parts ? mm : (mm * (uint64_t)(i + 1) / parts) & ~7ull;
-            part_bad[(size_t)i] = pack16(src + 2 * lo, dst + lo, hi - lo, base, (uint32_t)ybase, wcheck, qmax);
-        });
+        std::fill(part_bad.begin(), part_bad.end(), 0u);
+        pool->run(
+            [&](int i) {
+                const uint64_t lo = (mm * (uint64_t)i / parts) & ~7ull;
+                const uint64_t hi = i + 1 == parts ? mm : (mm * (uint64_t)(i + 1) / parts) & ~7ull;
+                part_bad[(size_t)i] = pack_any(in, front + lo, hi - lo, dst + lo, base, (uint32_t)ybase, wcheck, qmax);
+            },
+            parts);
         const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         if (mm >= (1u << 20) && dt > 0) ctx->pack_rate = 0.5 * ctx->pack_rate + 0.5 * (double)mm / dt;
         uint32_t chunk_bad = 0;
@@ -411,40 +468,27 @@ int stream_chunks_packed(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t 
             return rc;
         front += mm;
     }
-    *bad = any_bad != 0;
+    *bad = (any_bad | narrow_bad) != 0;
     return CHP_OK;
 }
 
-// A 2^16 x 2^16 packing window from the box of the first min(n, 1 Mi)
-// points (host pool), centred in the slack; false when that prefix is
-// already wider or taller than 2^16.
-bool pack_window(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t* wx, int64_t* wy) {
-    const uint64_t m = std::min<uint64_t>(n, 1ull << 20);
-    HostPool* pool = pool_of(ctx);
-    const int parts = pool->parts();
-    std::vector<int32_t> part((size_t)parts * 4);
-    pool->run([&](int i) {
-        int32_t b[4] = {INT32_MAX, INT32_MIN, INT32_MAX, INT32_MIN};
-        const uint64_t lo = m * (uint64_t)i / parts, hi = m * (uint64_t)(i + 1) / parts;
-        for (uint64_t k = lo; k < hi; ++k) {
-            const int32_t x = h_xy[2 * k], y = h_xy[2 * k + 1];
-            b[0] = std::min(b[0], x);
-            b[1] = std::max(b[1], x);
-            b[2] = std::min(b[2], y);
-            b[3] = std::max(b[3], y);
-        }
-        std::memcpy(&part[(size_t)i * 4], b, sizeof b);
-    });
-    int64_t b[4] = {INT32_MAX, INT32_MIN, INT32_MAX, INT32_MIN};
-    for (int i = 0; i < parts; ++i) {
-        b[0] = std::min<int64_t>(b[0], part[(size_t)i * 4]);
-        b[1] = std::max<int64_t>(b[1], part[(size_t)i * 4 + 1]);
-        b[2] = std::min<int64_t>(b[2], part[(size_t)i * 4 + 2]);
-        b[3] = std::max<int64_t>(b[3], part[(size_t)i * 4 + 3]);
+// A 2^16 x 2^16 packing window from the box of the first min(n, 64 Ki)
+// points, centred in the slack; false when that prefix is already wider or
+// taller than 2^16.
+bool pack_window(chp_ctx* ctx, const HostPts& in, uint64_t n, int64_t* wx, int64_t* wy) {
+    (void)ctx;
+    const uint64_t m = std::min<uint64_t>(n, 1ull << 16);  // a 64 Ki-point prefix, on the caller's thread
+    int64_t b[4] = {INT64_MAX, INT64_MIN, INT64_MAX, INT64_MIN};
+    for (uint64_t k = 0; k < m; ++k) {
+        const int64_t x = in.x(k), y = in.y(k);
+        b[0] = std::min(b[0], x);
+        b[1] = std::max(b[1], x);
+        b[2] = std::min(b[2], y);
+        b[3] = std::max(b[3], y);
     }
     auto place = [](int64_t lo, int64_t hi, int64_t* base) {
         const int64_t ext = hi - lo + 1;
-        if (ext > 65536) return false;
+        if (ext > 65536 || lo < INT32_MIN || hi > INT32_MAX) return false;
         int64_t s = lo - (65536 - ext) / 2;
         s = std::max<int64_t>(s, INT32_MIN);
         s = std::min<int64_t>(s, (int64_t)INT32_MAX - 65535);
@@ -458,7 +502,7 @@ bool pack_window(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t* wx, int
 // valid y in [ybase, ybase + ycount) (ycount < 0: no upper bound).  Inputs
 // whose slots and y offsets fit 16 bits travel packed (half the PCIe bytes)
 // unless CHP_PIPELINE_NO_PACK is set in flags or the environment.
-int stream_reduce(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t width, int64_t ybase, int64_t ycount,
+int stream_reduce(chp_ctx* ctx, const HostPts& in, uint64_t n, int64_t width, int64_t ybase, int64_t ycount,
                   int64_t x_off, uint32_t flags) {
     auto launch = [&](const int32_t* d, uint64_t m) {
         return chp_reduce_yr(ctx, d, m, width, ybase, ycount, x_off, (int32_t*)ctx->dl.p,
@@ -473,12 +517,19 @@ int stream_reduce(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t width, 
                           !(flags & CHP_PIPELINE_NO_PACK) && !std::getenv("CHP_PIPELINE_NO_PACK") &&
                           x_off + 1 >= (int64_t)INT32_MIN && x_off <= (int64_t)INT32_MAX &&
                           ybase >= (int64_t)INT32_MIN && ybase <= (int64_t)INT32_MAX;
-    if (!packable) return stream_chunks(ctx, h_xy, n, launch);
-    const uint32_t wcheck = (uint32_t)std::min<int64_t>(width, (int64_t)INT32_MAX - x_off);
-    const uint32_t qmax = (uint32_t)std::min<int64_t>(speculative ? 65536 : ycount, (int64_t)INT32_MAX - ybase + 1);
     bool bad = false;
-    int rc = stream_chunks_packed(ctx, h_xy, n, x_off, (int32_t)ybase, wcheck, qmax, speculative, &bad, launch);
-    if (rc) return rc;
+    int rc;
+    if (!packable) {
+        uint32_t nb = 0;  // int64 input: a coordinate beyond int32
+        if ((rc = stream_chunks(ctx, in, n, launch, nullptr, &nb))) return rc;
+        bad = nb != 0;
+    } else {
+        const uint32_t wcheck = (uint32_t)std::min<int64_t>(width, (int64_t)INT32_MAX - x_off);
+        const uint32_t qmax =
+            (uint32_t)std::min<int64_t>(speculative ? 65536 : ycount, (int64_t)INT32_MAX - ybase + 1);
+        if ((rc = stream_chunks_packed(ctx, in, n, x_off, (int32_t)ybase, wcheck, qmax, speculative, &bad, launch)))
+            return rc;
+    }
     if (bad) {  // same outcome as the unpacked path: the error word of DL
         int32_t minus1 = -1;
         CHP_CUDA(ctx, cudaMemcpyAsync((int32_t*)ctx->dl.p + 2 * width, &minus1, 4, cudaMemcpyHostToDevice,
@@ -643,9 +694,9 @@ const char* chp_last_variant(const chp_ctx* ctx) { return ctx ? ctx->variant : "
 
 uint64_t chp_last_h2d_bytes(const chp_ctx* ctx) { return ctx ? ctx->h2d_bytes : 0; }
 
-int chp_pipeline_host(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t width, int64_t q,
-                      int32_t* h_Lpairs, uint64_t* h_occ, int32_t* h_chain, int64_t* h_s, int32_t* h_hull,
-                      int64_t* h_h) {
+static int pipeline_core(chp_ctx* ctx, const HostPts& in, uint64_t n, int64_t width, int64_t q,
+                         int32_t* h_Lpairs, uint64_t* h_occ, int32_t* h_chain, int64_t* h_s, int32_t* h_hull,
+                         int64_t* h_h) {
     if (!ctx) return CHP_EINVAL;
     ctx->h2d_bytes = 0;
     ctx->last_valid = false;
@@ -655,9 +706,25 @@ int chp_pipeline_host(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t wid
     int rc;
     if ((rc = chp_ensure(ctx, ctx->dl, chp_dl_len(width) * 4))) return rc;
     if ((rc = chp_dl_init(ctx, (int32_t*)ctx->dl.p, width))) return rc;
-    if ((rc = stream_reduce(ctx, h_xy, n, width, 1, q, 0, 0))) return rc;
+    if ((rc = stream_reduce(ctx, in, n, width, 1, q, 0, 0))) return rc;
     return finish_host(ctx, width, 0, 0, h_Lpairs, h_occ, h_chain, h_s, h_hull, h_h,
                        h_chain != nullptr || h_hull != nullptr);
+}
+
+int chp_pipeline_host(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t width, int64_t q,
+                      int32_t* h_Lpairs, uint64_t* h_occ, int32_t* h_chain, int64_t* h_s, int32_t* h_hull,
+                      int64_t* h_h) {
+    HostPts in;
+    in.p32 = h_xy;
+    return pipeline_core(ctx, in, n, width, q, h_Lpairs, h_occ, h_chain, h_s, h_hull, h_h);
+}
+
+int chp_pipeline_host64(chp_ctx* ctx, const int64_t* h_xy, uint64_t n, int64_t width, int64_t q,
+                        int32_t* h_Lpairs, uint64_t* h_occ, int32_t* h_chain, int64_t* h_s, int32_t* h_hull,
+                        int64_t* h_h) {
+    HostPts in;
+    in.p64 = h_xy;
+    return pipeline_core(ctx, in, n, width, q, h_Lpairs, h_occ, h_chain, h_s, h_hull, h_h);
 }
 
 int chp_translate_host(chp_ctx* ctx, const int32_t* h_in, uint64_t n, int32_t dx, int32_t dy, int32_t* h_out) {
@@ -711,7 +778,7 @@ int chp_polyline_host(chp_ctx* ctx, const int32_t* h_Lpairs, int64_t width, int6
     return CHP_OK;
 }
 
-static int precondition_core(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t* h_bbox4, bool bounds_only,
+static int precondition_core(chp_ctx* ctx, const HostPts& in, uint64_t n, int64_t* h_bbox4, bool bounds_only,
                              const std::function<int(int64_t width, int64_t x_off)>& finish) {
     if (!ctx) return CHP_EINVAL;
     ctx->h2d_bytes = 0;
@@ -723,10 +790,15 @@ static int precondition_core(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int6
     // computed as it lands; the buffer is kept in the context); otherwise
     // they are streamed twice.
     int rc;
-    size_t freeb = 0, totalb = 0;
-    CHP_CUDA(ctx, cudaMemGetInfo(&freeb, &totalb));
-    // (CHP_PRECONDITION_STREAM forces the streamed form: tests only.)
-    const bool resident = (size_t)n * 8 <= (freeb + ctx->points.bytes) / 4 && !std::getenv("CHP_PRECONDITION_STREAM");
+    // (cudaMemGetInfo costs 0.1-0.4 ms: only asked when the held buffer is
+    // too small.  CHP_PRECONDITION_STREAM forces the streamed form: tests.)
+    bool resident = (size_t)n * 8 <= ctx->points.bytes;
+    if (!resident) {
+        size_t freeb = 0, totalb = 0;
+        CHP_CUDA(ctx, cudaMemGetInfo(&freeb, &totalb));
+        resident = (size_t)n * 8 <= (freeb + ctx->points.bytes) / 4;
+    }
+    if (std::getenv("CHP_PRECONDITION_STREAM")) resident = false;
     DevBuf& pts = ctx->points;
     if ((rc = chp_ensure(ctx, ctx->counts, 16 * sizeof(int64_t)))) return rc;
     int32_t* d_b4 = (int32_t*)((int64_t*)ctx->counts.p + 8);
@@ -736,28 +808,33 @@ static int precondition_core(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int6
         if ((rc = chp_bounds_init(ctx, d_b4))) return rc;
         auto fold = [&](const int32_t* d, uint64_t m) { return chp_bounds_accumulate(ctx, d, m, d_b4); };
         // The box is unknown until every point has been seen, so the 16-bit
-        // packing is speculative: a window sized from the first 1 Mi points'
+        // packing is speculative: a window sized from the first 64 Ki points'
         // box (centred in the 2^16 slack) packs every chunk that fits, the
         // rest travel as int32 pairs; either way they land unpacked in the
         // resident buffer.
         int64_t wx = 0, wy = 0;
-        const bool win = !std::getenv("CHP_PIPELINE_NO_PACK") && pack_window(ctx, h_xy, n, &wx, &wy);
+        const bool win = !std::getenv("CHP_PIPELINE_NO_PACK") && pack_window(ctx, in, n, &wx, &wy);
+        bool narrow_bad = false;  // int64 input: a coordinate beyond int32
         if (win) {
-            bool unused = false;
-            if ((rc = stream_chunks_packed(ctx, h_xy, n, wx - 1, (int32_t)wy, 65536u, 65536u, true, &unused, fold,
+            if ((rc = stream_chunks_packed(ctx, in, n, wx - 1, (int32_t)wy, 65536u, 65536u, true, &narrow_bad, fold,
                                            (int32_t*)pts.p)))
                 return rc;
-        } else if ((rc = stream_chunks(ctx, h_xy, n, fold, (int32_t*)pts.p))) {
-            return rc;
+        } else {
+            uint32_t nb = 0;
+            if ((rc = stream_chunks(ctx, in, n, fold, (int32_t*)pts.p, &nb))) return rc;
+            narrow_bad = nb != 0;
         }
+        if (narrow_bad) return chp_einval(ctx, "precondition: coordinate does not fit int32");
         CHP_CUDA(ctx, cudaMemcpyAsync(b4, d_b4, 16, cudaMemcpyDeviceToHost, ctx->stream));
         CHP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     } else {
         if ((rc = chp_bounds_init(ctx, d_b4))) return rc;
-        if ((rc = stream_chunks(ctx, h_xy, n, [&](const int32_t* d, uint64_t m) {
-                 return chp_bounds_accumulate(ctx, d, m, d_b4);
-             })))
+        uint32_t nb = 0;
+        if ((rc = stream_chunks(
+                 ctx, in, n, [&](const int32_t* d, uint64_t m) { return chp_bounds_accumulate(ctx, d, m, d_b4); },
+                 nullptr, &nb)))
             return rc;
+        if (nb) return chp_einval(ctx, "precondition: coordinate does not fit int32");
         CHP_CUDA(ctx, cudaMemcpyAsync(b4, d_b4, 16, cudaMemcpyDeviceToHost, ctx->stream));
         CHP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     }
@@ -783,7 +860,7 @@ static int precondition_core(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int6
         rc = chp_reduce_yr(ctx, (const int32_t*)pts.p, n, width, ybase, ycount, x_off, (int32_t*)ctx->dl.p, rflags);
     } else {
         rc = chp_dl_init(ctx, (int32_t*)ctx->dl.p, width);
-        if (!rc) rc = stream_reduce(ctx, h_xy, n, width, ybase, ycount, x_off, rflags);
+        if (!rc) rc = stream_reduce(ctx, in, n, width, ybase, ycount, x_off, rflags);
     }
     if (rc) return rc;
     return finish(width, x_off);
@@ -793,16 +870,18 @@ static int precondition_core(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int6
 int chp_precondition_host(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t* h_bbox4, int32_t* h_Lpairs,
                           int32_t* h_chain, int64_t* h_s, int32_t* h_hull, int64_t* h_h) {
     const bool bounds_only = !h_chain && !h_hull && !h_s && !h_Lpairs && !h_h;
-    return precondition_core(ctx, h_xy, n, h_bbox4, bounds_only, [&](int64_t width, int64_t x_off) {
+    HostPts in;
+    in.p32 = h_xy;
+    return precondition_core(ctx, in, n, h_bbox4, bounds_only, [&](int64_t width, int64_t x_off) {
         return finish_host(ctx, width, x_off, 0, h_Lpairs, nullptr, h_chain, h_s, h_hull, h_h, true);
     });
 }
 
-int chp_precondition_run(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int want_hull, int64_t* h_bbox4,
-                         int64_t* h_width, int64_t* h_s, int64_t* h_h) {
+static int precondition_run_core(chp_ctx* ctx, const HostPts& in, uint64_t n, int want_hull, int64_t* h_bbox4,
+                                 int64_t* h_width, int64_t* h_s, int64_t* h_h) {
     if (ctx) ctx->last_valid = false;
     int64_t width = 0, s = 0, h = 0;
-    const int rc = precondition_core(ctx, h_xy, n, h_bbox4, false, [&](int64_t w, int64_t x_off) {
+    const int rc = precondition_core(ctx, in, n, h_bbox4, false, [&](int64_t w, int64_t x_off) {
         int64_t cnt[8];
         int r = finish_device(ctx, w, x_off, 0, true, true, false, want_hull != 0, cnt);
         if (r) return r;
@@ -822,6 +901,28 @@ int chp_precondition_run(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int want
     if (h_s) *h_s = s;
     if (h_h) *h_h = want_hull ? h : 0;
     return CHP_OK;
+}
+
+int chp_precondition_run(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int want_hull, int64_t* h_bbox4,
+                         int64_t* h_width, int64_t* h_s, int64_t* h_h) {
+    HostPts in;
+    in.p32 = h_xy;
+    return precondition_run_core(ctx, in, n, want_hull, h_bbox4, h_width, h_s, h_h);
+}
+
+int chp_precondition_run64(chp_ctx* ctx, const int64_t* h_xy, uint64_t n, int swap_axes, int want_hull,
+                           int64_t* h_bbox4, int64_t* h_width, int64_t* h_s, int64_t* h_h) {
+    HostPts in;
+    in.p64 = h_xy;
+    in.swap = swap_axes != 0;
+    return precondition_run_core(ctx, in, n, want_hull, h_bbox4, h_width, h_s, h_h);
+}
+
+int chp_bounds_host64(chp_ctx* ctx, const int64_t* h_xy, uint64_t n, int64_t* h_bbox4) {
+    HostPts in;
+    in.p64 = h_xy;
+    // K0 on the device over the narrowed points (bounds only)
+    return precondition_core(ctx, in, n, h_bbox4, true, [](int64_t, int64_t) { return CHP_OK; });
 }
 
 int chp_last_outputs(chp_ctx* ctx, int32_t* h_Lpairs, int32_t* h_chain, int32_t* h_hull) {

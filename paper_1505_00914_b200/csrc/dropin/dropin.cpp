@@ -80,9 +80,16 @@ std::vector<Point> widen(const int32_t* xy, int64_t n, bool swap = false) {
     return out;
 }
 
-BoundingBox bounds_of(const std::vector<int32_t>& xy) {
+// The reference's Point is two int64 words: the int64 entry points read
+// the caller's array directly (no narrowed copy on the host).
+const int64_t* raw64(std::span<const Point> pts) {
+    static_assert(sizeof(Point) == 2 * sizeof(int64_t), "Point must be two packed int64");
+    return reinterpret_cast<const int64_t*>(pts.data());
+}
+
+BoundingBox bounds_of(std::span<const Point> pts) {
     int64_t b4[4] = {0, 0, 0, 0};
-    check(chp_precondition_host(ctx(), xy.data(), xy.size() / 2, b4, nullptr, nullptr, nullptr, nullptr, nullptr));
+    check(chp_bounds_host64(ctx(), raw64(pts), pts.size(), b4));
     return {b4[0], b4[1], b4[2], b4[3]};
 }
 
@@ -120,17 +127,15 @@ occupancy::Index index_from_entries(const std::vector<reducer::ColumnExtremes>& 
 // along y.
 Hull device_hull(std::span<const Point> pts) {
     if (pts.empty()) throw std::invalid_argument("hull: empty input");
-    auto xy = narrow(pts);
     int64_t b4[4] = {0, 0, 0, 0}, w = 0, s = 0, h = 0;
-    int rc = chp_precondition_run(ctx(), xy.data(), xy.size() / 2, 1, b4, &w, &s, &h);
+    int rc = chp_precondition_run64(ctx(), raw64(pts), pts.size(), 0, 1, b4, &w, &s, &h);
     bool swap = false;
     if (rc == CHP_EINVAL && b4[1] - b4[0] + 1 > (1ll << 29)) {
         const BoundingBox bb{b4[0], b4[1], b4[2], b4[3]};
         if (bb.height() > (1ll << 29) || bb.height() >= bb.width())
             throw std::invalid_argument("hull: point extent exceeds the device limit 2^29");
         swap = true;
-        xy = narrow(pts, true);
-        rc = chp_precondition_run(ctx(), xy.data(), xy.size() / 2, 1, b4, &w, &s, &h);
+        rc = chp_precondition_run64(ctx(), raw64(pts), pts.size(), 1, 1, b4, &w, &s, &h);
     }
     check(rc);
     std::vector<int32_t> hull(2 * static_cast<size_t>(h));
@@ -151,7 +156,7 @@ Hull device_hull(std::span<const Point> pts) {
 
 BoundingBox find_bounds(std::span<const Point> points) {
     if (points.empty()) throw std::invalid_argument("find_bounds: empty input");
-    return detail::bounds_of(detail::narrow(points));
+    return detail::bounds_of(points);
 }
 
 namespace {
@@ -217,7 +222,7 @@ namespace kernels {
 
 MinMax min_max(std::span<const Point> pts) {
     if (pts.empty()) throw std::invalid_argument("min_max: empty input");
-    const BoundingBox b = detail::bounds_of(detail::narrow(pts));
+    const BoundingBox b = detail::bounds_of(pts);
     return {b.x_min, b.x_max, b.y_min, b.y_max};
 }
 
@@ -283,13 +288,12 @@ std::vector<Point> translate(std::span<const Point> points, const BoundingBox& b
 ExtremalArray reduce(std::span<const Point> points, std::int64_t width, std::optional<std::int64_t> q,
                      occupancy::Kind occ_kind) {
     if (width < 1) throw std::invalid_argument("reduce: width must be >= 1");
-    auto xy = detail::narrow(points);
     std::vector<int32_t> L(2 * static_cast<size_t>(width));
     std::vector<std::uint64_t> words((static_cast<size_t>(width) + 63) / 64);
     int64_t s = 0;
     const int64_t qq = q ? std::max<int64_t>(*q, 0) : -1;
-    detail::check(chp_pipeline_host(detail::ctx(), xy.data(), points.size(), width, qq, L.data(), words.data(),
-                                    nullptr, &s, nullptr, nullptr));
+    detail::check(chp_pipeline_host64(detail::ctx(), detail::raw64(points), points.size(), width, qq, L.data(),
+                                      words.data(), nullptr, &s, nullptr, nullptr));
     ExtremalArray arr{detail::entries_from_pairs(L), occupancy::Index(static_cast<std::uint64_t>(width), occ_kind)};
     arr.occ.assign_words(words.data(), words.size());
     return arr;
@@ -341,19 +345,19 @@ PreconditionResult precondition(std::span<const Point> points, const Preconditio
     if (points.empty()) throw std::invalid_argument("precondition: empty input");
     using clock = std::chrono::steady_clock;
     auto t0 = clock::now();
-    auto xy = detail::narrow(points);
     const bool full_bounds = options.second_scan || options.auto_axis;
     // auto_axis needs the box before choosing the axis (one bounds-only pass);
-    // otherwise bounds, fold, compaction are ONE pass (chp_precondition_run).
+    // otherwise bounds, fold, compaction are ONE pass over the caller's int64
+    // points (chp_precondition_run64).
     bool swap = false;
     if (options.auto_axis) {
-        const BoundingBox bb0 = detail::bounds_of(xy);
+        const BoundingBox bb0 = detail::bounds_of(points);
         swap = bb0.height() < bb0.width();
-        if (swap) xy = detail::narrow(points, true);
     }
     auto t1 = clock::now();
     int64_t b4[4] = {0, 0, 0, 0}, width = 0, s = 0;
-    const int rc = chp_precondition_run(detail::ctx(), xy.data(), points.size(), 0, b4, &width, &s, nullptr);
+    const int rc = chp_precondition_run64(detail::ctx(), detail::raw64(points), points.size(), swap ? 1 : 0, 0, b4,
+                                          &width, &s, nullptr);
     if (rc == CHP_EINVAL && b4[1] - b4[0] + 1 > (1ll << 29))
         throw std::invalid_argument("precondition: extent exceeds the device limit 2^29");
     detail::check(rc);

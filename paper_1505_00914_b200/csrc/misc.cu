@@ -56,11 +56,33 @@ __global__ void __launch_bounds__(512) k_bounds(const int32_t* __restrict__ xy, 
         ymin = min(ymin, __shfl_xor_sync(0xffffffffu, ymin, o));
         ymax = max(ymax, __shfl_xor_sync(0xffffffffu, ymax, o));
     }
+    // Block reduction, then one atomic per word per block (per-warp atomics
+    // on four addresses serialised at L2: 28 us for 1 M points).
+    __shared__ int red[4][16];
+    const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     if ((threadIdx.x & 31) == 0) {
-        atomicMin(out4 + 0, xmin);
-        atomicMax(out4 + 1, xmax);
-        atomicMin(out4 + 2, ymin);
-        atomicMax(out4 + 3, ymax);
+        red[0][warp] = xmin;
+        red[1][warp] = xmax;
+        red[2][warp] = ymin;
+        red[3][warp] = ymax;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const int l = threadIdx.x;
+        int a = l < nw ? red[0][l] : INT_MAX, b = l < nw ? red[1][l] : INT_MIN;
+        int c = l < nw ? red[2][l] : INT_MAX, d = l < nw ? red[3][l] : INT_MIN;
+        for (int o = 8; o > 0; o >>= 1) {
+            a = min(a, __shfl_xor_sync(0xffffffffu, a, o));
+            b = max(b, __shfl_xor_sync(0xffffffffu, b, o));
+            c = min(c, __shfl_xor_sync(0xffffffffu, c, o));
+            d = max(d, __shfl_xor_sync(0xffffffffu, d, o));
+        }
+        if (l == 0) {
+            atomicMin(out4 + 0, a);
+            atomicMax(out4 + 1, b);
+            atomicMin(out4 + 2, c);
+            atomicMax(out4 + 3, d);
+        }
     }
 }
 

@@ -203,7 +203,7 @@ def test_pipeline_host_q_unset_invalid(ctx, pinned, bad):
 
 @pytest.mark.parametrize("pinned", [False, True])
 def test_precondition_speculative_window(ctx, orc, pinned):
-    # The packing window comes from the first 1 Mi points; later chunks that
+    # The packing window comes from the first 64 Ki points; later chunks that
     # leave it (here: x and y spread 4x wider after 9 M points) go as int32.
     rng = np.random.default_rng(77)
     n = 20_000_000
