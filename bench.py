@@ -377,7 +377,8 @@ def main():
             precondition_e2e = {"value": n / (pre_ms * 1e-3) / 1e9, "unit": "Gpoints/s", "ms_per_step": pre_ms,
                                 "h2d_bytes_per_step": ctx.last_h2d_bytes,
                                 "path": "chp_precondition_run + chp_last_outputs (pinned int32 input, bounds "
-                                        "unknown: one pass with the bounds folded as the chunks land)"}
+                                        "unknown: one pass, speculative 16-bit packing against a window from a "
+                                        "64 Ki-point prefix, the bounds folded as the chunks land)"}
         del host
 
     base = None
