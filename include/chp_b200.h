@@ -95,6 +95,7 @@ uint64_t chp_dl_len(int64_t width);
 #define CHP_REDUCE_SAMPLE_TMA (1u << 22) /* tuning: sample pass streams through the TMA ring */
 #define CHP_PIPELINE_NO_PACK (1u << 23) /* host pipelines: always send int32 pairs (no 16-bit packing) */
 #define CHP_REDUCE_SAMPLE_SPLIT (1u << 25) /* tuning: sampled filter's sample pass and merge as separate launches */
+#define CHP_REDUCE_BLOCKED (1u << 26) /* tuning: smem/filter streams in per-CTA contiguous slices (the sampled main pass always is) */
 
 /* Algorithm 1 over n int32 (x,y) pairs at d_xy (8-byte aligned).  Slot of a
  * point is x - x_off - 1; a point is valid when that slot is in [0,width)

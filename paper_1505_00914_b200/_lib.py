@@ -22,6 +22,7 @@ REDUCE_FORCE_SMEM16 = 64
 REDUCE_FORCE_SAMPLED = 8192
 REDUCE_FUSED = 16384
 REDUCE_SAMPLE_SPLIT = 1 << 25
+REDUCE_BLOCKED = 1 << 26
 
 _lib = None
 

@@ -34,6 +34,8 @@ VARIANTS = {
     "filter_read_tma": _lib.REDUCE_FORCE_FILTER | 256 | 4096,
     "sampled_tma": _lib.REDUCE_FORCE_SAMPLED | 4096,
     "sampled_split": _lib.REDUCE_FORCE_SAMPLED | _lib.REDUCE_SAMPLE_SPLIT,
+    "smem16_blocked": _lib.REDUCE_FORCE_SMEM16 | _lib.REDUCE_BLOCKED,
+    "filter_blocked": _lib.REDUCE_FORCE_FILTER | _lib.REDUCE_BLOCKED,
 }
 
 
