@@ -525,8 +525,12 @@ __global__ void __launch_bounds__(256) k_filter_build(const int* __restrict__ DL
 // F == nullptr starts from an all-"never skip" table (the warm-up pass:
 // every point is settled in L2, building the first snapshot).  Validated
 // input only (y in [1, q]); the host guarantees wcheck == width.
+// The read-first register form runs 896 threads per CTA: its miss batches
+// plus the load pipeline need more than 64 registers per thread (at 1024
+// threads it spilled 32 B; C4: 768 656, 896 663, 1024 657 Gpts/s).
+constexpr int kThreadsRF = 896;
 template <typename W, bool READ_FIRST, bool TMA>
-__global__ void __launch_bounds__(kThreads) k_reduce_filter(const int32_t* __restrict__ xy, uint64_t n,
+__global__ void __launch_bounds__((READ_FIRST && !TMA) ? kThreadsRF : kThreads) k_reduce_filter(const int32_t* __restrict__ xy, uint64_t n,
                                                             Geo g, uint32_t width, uint32_t gshift, uint32_t ys,
                                                             const W* __restrict__ F, uint32_t ngroups, int stages,
                                                             int* __restrict__ DL) {
@@ -1167,7 +1171,15 @@ int run_group_filter(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, const Geo& g
     uint64_t cur_done = 0;  // first point of the phase being launched
     auto pass = [&](const int32_t* xy, uint64_t cnt, const W* F) {
         const bool rf = force_read || (!force_red && cur_done < read_until);
-        if (rf)
+        if (rf && !pl.tma) {
+            auto fn = k_reduce_filter<W, true, false>;
+            CHP_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+            int per_sm = 0;
+            CHP_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreadsRF, pl.smem));
+            fn<<<std::max(1, std::min(per_sm, 2)) * ctx->sm_count, kThreadsRF, pl.smem, ctx->stream>>>(
+                xy, cnt, g, w, gshift, ys, F, ngroups, pl.stages, d_L);
+            CHP_LAUNCHED(ctx);
+        } else if (rf)
             CHP_LAUNCH_PLANNED(ctx, pl, (k_reduce_filter<W, true, true>), (k_reduce_filter<W, true, false>), xy, cnt,
                                g, w, gshift, ys, F, ngroups, pl.stages, d_L);
         else
