@@ -57,7 +57,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     procs = []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
-        cmd = [nvcc()] + NVCC_FLAGS + ["-c", src, "-o", obj]
+        # CHP_NVCC_EXTRA: instrumentation builds only (e.g. -DCHP_PHASE_TIMING=1, tools/phase_timing.py)
+        cmd = [nvcc()] + NVCC_FLAGS + os.environ.get("CHP_NVCC_EXTRA", "").split() + ["-c", src, "-o", obj]
         if src.endswith(".cpp"):  # host-only C++ over the C ABI
             cmd = [os.environ.get("CXX", "g++"), "-O3", "-std=c++20", "-fPIC", "-Wall", "-I" + INCLUDE,
                    "-c", src, "-o", obj]

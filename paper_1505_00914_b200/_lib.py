@@ -23,6 +23,7 @@ REDUCE_FORCE_SAMPLED = 8192
 REDUCE_FUSED = 16384
 REDUCE_SAMPLE_SPLIT = 1 << 25
 REDUCE_BLOCKED = 1 << 26
+REDUCE_SAMPLE_PREFIX = 1 << 27
 
 _lib = None
 

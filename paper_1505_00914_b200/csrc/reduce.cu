@@ -42,6 +42,25 @@ namespace {
 
 constexpr int kThreads = 1024;
 
+// Instrumentation build only (CHP_NVCC_EXTRA=-DCHP_PHASE_TIMING=1, read by
+// tools/phase_timing.py): thread 0 of every CTA stamps %globaltimer at the
+// sampled pipeline's phase boundaries.
+#ifndef CHP_PHASE_TIMING
+#define CHP_PHASE_TIMING 0
+#endif
+#if CHP_PHASE_TIMING
+__device__ unsigned long long g_phase[160][8];
+__device__ __forceinline__ void phase_mark(int k) {
+    if (threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_phase[blockIdx.x][k] = t;
+    }
+}
+#else
+__device__ __forceinline__ void phase_mark(int) {}
+#endif
+
 struct Geo {
     uint32_t base;    // x_off + 1 (mod 2^32): slot = x - base
     uint32_t wcheck;  // slots reachable by an int32 x: min(width, INT_MAX - x_off)
@@ -655,9 +674,16 @@ __device__ __forceinline__ void sample_init(uint4* smem4, uint32_t wpad, int* __
 // invalid x lands in the sink slot `width` (never merged), an invalid y can
 // only garble its own column's word, and the main pass, which sees every
 // point again, fails the call.
+//
+// The sample is n * f256 / 256 points: by default the head of every CTA's
+// main-pass slice (for_each_group_pp's [vb, ve)); `prefix` (and the TMA form)
+// take the first n * f256 / 256 points instead.  The heads spread the sample
+// over the whole input (an input sorted by x or y still yields a table for
+// every part of it); on C2 the two measure the same.
 template <bool TMA>
-__device__ __forceinline__ void sample_fold(const int32_t* __restrict__ xy, uint64_t n, const Geo& g,
-                                            uint32_t width, uint32_t ys, uint16_t* T, uint8_t* ring, int stages) {
+__device__ __forceinline__ void sample_fold(const int32_t* __restrict__ xy, uint64_t n, uint32_t f256, bool prefix,
+                                            const Geo& g, uint32_t width, uint32_t ys, uint16_t* T, uint8_t* ring,
+                                            int stages) {
     auto f = [&](int32_t x, int32_t y) {
         const uint32_t s = min(slot_of(x, g.base), width);
         const uint32_t u = ((uint32_t)y - g.ybase) >> ys;
@@ -666,7 +692,8 @@ __device__ __forceinline__ void sample_fold(const int32_t* __restrict__ xy, uint
         if (nw != w) T[s] = (uint16_t)nw;
     };
     if (TMA) {
-        stream_points<true>(xy, n, ring, stages, per_point4(f), f);
+        const uint64_t ns = n * f256 >> 8;
+        stream_points<true>(xy, ns > 2 ? ns : (n < 2 ? n : 2), ring, stages, per_point4(f), f);
         return;
     }
     // Each thread sees only ~80 sample points, so the pass is bound by
@@ -674,10 +701,19 @@ __device__ __forceinline__ void sample_fold(const int32_t* __restrict__ xy, uint
     // once (3 round trips instead of 10 for the C2 sample).
     const Split sp = split_points(xy, n);
     const int4* __restrict__ v = reinterpret_cast<const int4*>(xy + 2 * sp.head);
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    uint64_t stride, i, end;
+    if (prefix) {
+        stride = (uint64_t)gridDim.x * blockDim.x;
+        i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+        end = sp.nvec * f256 >> 8;
+    } else {
+        const uint64_t vb = sp.nvec * blockIdx.x / gridDim.x, ve = sp.nvec * (blockIdx.x + 1) / gridDim.x;
+        stride = blockDim.x;
+        i = vb + threadIdx.x;
+        end = vb + ((ve - vb) * f256 >> 8);
+    }
     constexpr int kB = 16;  // loads issued per batch (C2: 8 575.6, 12 577.3, 16 578.5 Gpts/s)
-    for (; i + (kB - 1) * stride < sp.nvec; i += kB * stride) {
+    for (; i + (kB - 1) * stride < end; i += kB * stride) {
         int4 q[kB];
 #pragma unroll
         for (int j = 0; j < kB; ++j) q[j] = ld_stream(v + i + j * stride);
@@ -687,7 +723,7 @@ __device__ __forceinline__ void sample_fold(const int32_t* __restrict__ xy, uint
             f(q[j].z, q[j].w);
         }
     }
-    for (; i < sp.nvec; i += stride) {
+    for (; i < end; i += stride) {
         const int4 a = ld_stream(v + i);
         f(a.x, a.y);
         f(a.z, a.w);
@@ -749,13 +785,13 @@ template <bool TMA>
 __global__ void __launch_bounds__(kThreads) k_sample_learn(const int32_t* __restrict__ xy, uint64_t n, Geo g,
                                                            uint32_t width, uint32_t wpad, uint32_t ys,
                                                            uint16_t* __restrict__ scratch, int* __restrict__ DL,
-                                                           int init_dl, int stages) {
+                                                           int init_dl, int stages, uint32_t f256, int prefix) {
     extern __shared__ uint4 smem4[];
     uint8_t* ring = reinterpret_cast<uint8_t*>(smem4) + table_span((size_t)wpad * 2);
     pdl_trigger();  // the merge may queue (it cannot co-reside; it waits)
     sample_init(smem4, wpad, DL, width, init_dl);
     __syncthreads();
-    sample_fold<TMA>(xy, n, g, width, ys, reinterpret_cast<uint16_t*>(smem4), ring, stages);
+    sample_fold<TMA>(xy, n, f256, prefix != 0, g, width, ys, reinterpret_cast<uint16_t*>(smem4), ring, stages);
     __syncthreads();
     sample_dump(smem4, scratch, wpad);
 }
@@ -893,12 +929,17 @@ __global__ void __launch_bounds__(kThreads) k_reduce_sampled(const int32_t* __re
     uint8_t* ring = reinterpret_cast<uint8_t*>(smem4) + table_span((size_t)wpad * 2);
     pdl_trigger();
     pdl_wait();  // the merged table (and DL, initialised by the sample pass)
+    phase_mark(6);
     {
         const uint4* F4 = reinterpret_cast<const uint4*>(F);
         for (uint32_t i = threadIdx.x; i < wpad / 8; i += blockDim.x) smem4[i] = __ldcg(F4 + i);
     }
     __syncthreads();
     sampled_pass<TMA>(xy, n, g, width, ys, (uint32_t)__cvta_generic_to_shared(smem4), ring, stages, DL);
+    if (CHP_PHASE_TIMING) {
+        __syncthreads();
+        phase_mark(7);
+    }
 }
 
 // ------------------------------------------------------- sampled, fused
@@ -941,7 +982,8 @@ __device__ __noinline__ void sampled_main_pass(const int32_t* __restrict__ xy, u
     sampled_pass<false>(xy, n, g, width, ys, tbase, nullptr, 0, DL);
 }
 
-__global__ void __launch_bounds__(kThreads) k_sampled_fused(const int32_t* __restrict__ xy, uint64_t n, uint64_t ns,
+__global__ void __launch_bounds__(kThreads) k_sampled_fused(const int32_t* __restrict__ xy, uint64_t n, uint32_t f256,
+                                                            int prefix,
                                                             Geo g, uint32_t width, uint32_t wpad, uint32_t ys,
                                                             uint16_t* __restrict__ scratch, uint16_t* __restrict__ F,
                                                             int* __restrict__ DL, int init_dl, GridBar* bar,
@@ -949,13 +991,18 @@ __global__ void __launch_bounds__(kThreads) k_sampled_fused(const int32_t* __res
     extern __shared__ uint4 smem4[];
     const uint32_t nchunks = wpad / 8;
     if (merge_only) pdl_trigger();  // the main pass (a dependent launch) may queue
+    phase_mark(0);
     // ---- A: sample pass + DL init
     sample_init(smem4, wpad, DL, width, init_dl);
     __syncthreads();
-    sample_fold<false>(xy, ns, g, width, ys, reinterpret_cast<uint16_t*>(smem4), nullptr, 0);
+    phase_mark(1);
+    sample_fold<false>(xy, n, f256, prefix != 0, g, width, ys, reinterpret_cast<uint16_t*>(smem4), nullptr, 0);
     __syncthreads();
+    phase_mark(2);
     sample_dump(smem4, scratch, wpad);
+    phase_mark(3);
     grid_barrier(bar);
+    phase_mark(4);
     // ---- B: merge; this CTA owns chunks [c0, c1), 64 chunks x 16 slices
     {
         const uint32_t per = (nchunks + gridDim.x - 1) / gridDim.x;
@@ -988,6 +1035,7 @@ __global__ void __launch_bounds__(kThreads) k_sampled_fused(const int32_t* __res
             __syncthreads();
         }
     }
+    phase_mark(5);
     if (merge_only) return;  // the main pass is a separate (dependent) launch
     grid_barrier(bar);
     // ---- C: every CTA loads the merged table
@@ -1340,7 +1388,7 @@ int chp_reduce_yr(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t width, 
             return CHP_OK;
         }
         case V_SAMPLED: {
-            // Sample pass (prefix n/8) -> merged strict-interior table -> one
+            // Sample pass (n/16) -> merged strict-interior table -> one
             // pass over all n points.
             uint32_t ys = 0;
             while ((uint64_t)(q - 1) >> ys > 254) ++ys;
@@ -1349,10 +1397,14 @@ int chp_reduce_yr(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t width, 
             int rc = chp_ensure(ctx, ctx->sample, (size_t)sblocks * tbytes + 16);
             if (!rc) rc = chp_ensure(ctx, ctx->filter, tbytes + 16);
             if (rc) return rc;
-            // Sample = the first n / 2^k points; k = 3 unless CHP_REDUCE_SAMPLE_K(k)
-            // (C2: k=3 510.7, k=4 505.2, k=5 474.4, k=6 430.0 Gpts/s).
-            const uint32_t kshift = (flags >> 16) & 7 ? (flags >> 16) & 7 : 3;
-            const uint64_t ns = std::min<uint64_t>(n, std::max<uint64_t>(n >> kshift, 2)) & ~1ull;
+            // Sample = n / 2^k points, k = 4 unless CHP_REDUCE_SAMPLE_K(k): the
+            // heads of the main pass's per-CTA slices, or the prefix
+            // (CHP_REDUCE_SAMPLE_PREFIX).  C2, same box: n * 32/256 585-590,
+            // 24/256 596, 20/256 612, 16/256 631, 14/256 638, 12/256 619,
+            // 10/256 620, 8/256 600 Gpts/s (k = 3 had been best before the
+            // main pass got cheaper per point).
+            uint32_t f256 = 256u >> ((flags >> 16) & 7 ? (flags >> 16) & 7 : 4);
+            int prefix = (flags & CHP_REDUCE_SAMPLE_PREFIX) ? 1 : 0;
             // Default: sample pass + merge as ONE cooperative kernel (a grid
             // barrier between them, the merge spread over every CTA), then the
             // main pass as a dependent launch (C2: 586 vs 573 Gpts/s for
@@ -1376,7 +1428,7 @@ int chp_reduce_yr(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t width, 
                     uint16_t* scratch = (uint16_t*)ctx->sample.p;
                     uint16_t* F = (uint16_t*)ctx->filter.p;
                     GridBar* bar = (GridBar*)ctx->gridbar.p;
-                    void* args[] = {(void*)&d_xy, (void*)&n,     (void*)&ns, (void*)&g,   (void*)&w,   (void*)&wpad8,
+                    void* args[] = {(void*)&d_xy, (void*)&n, (void*)&f256, (void*)&prefix, (void*)&g, (void*)&w, (void*)&wpad8,
                                     (void*)&ys,   (void*)&scratch, (void*)&F, (void*)&d_L, (void*)&init, (void*)&bar,
                                     (void*)&merge_only};
                     // (A cooperative launch can be refused when the GPU is
@@ -1406,8 +1458,8 @@ int chp_reduce_yr(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t width, 
                 auto fn = sp.tma ? k_sample_learn<true> : k_sample_learn<false>;
                 int unused = 0;
                 if ((rc = kernel_blocks(ctx, (const void*)fn, sp.smem, 1, &unused))) return rc;
-                fn<<<sblocks, kThreads, sp.smem, ctx->stream>>>(d_xy, ns, g, w, wpad8, ys, (uint16_t*)ctx->sample.p,
-                                                                d_L, need_init ? 1 : 0, sp.stages);
+                fn<<<sblocks, kThreads, sp.smem, ctx->stream>>>(d_xy, n, g, w, wpad8, ys, (uint16_t*)ctx->sample.p,
+                                                                d_L, need_init ? 1 : 0, sp.stages, f256, prefix);
                 CHP_LAUNCHED(ctx);
             }
             const uint32_t nchunks = wpad8 / 8;
@@ -1455,3 +1507,9 @@ extern "C" int chp_check(chp_ctx* ctx, const int32_t* d_L, int64_t width) {
     if (err != 0) return chp_einval(ctx, "reduce: coordinate out of range");
     return CHP_OK;
 }
+
+#if CHP_PHASE_TIMING
+extern "C" int chp_debug_phase(unsigned long long* out) {
+    return (int)cudaMemcpyFromSymbol(out, g_phase, sizeof(g_phase));
+}
+#endif

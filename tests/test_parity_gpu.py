@@ -36,6 +36,8 @@ VARIANTS = {
     "sampled_split": _lib.REDUCE_FORCE_SAMPLED | _lib.REDUCE_SAMPLE_SPLIT,
     "smem16_blocked": _lib.REDUCE_FORCE_SMEM16 | _lib.REDUCE_BLOCKED,
     "filter_blocked": _lib.REDUCE_FORCE_FILTER | _lib.REDUCE_BLOCKED,
+    "sampled_prefix": _lib.REDUCE_FORCE_SAMPLED | _lib.REDUCE_SAMPLE_PREFIX,
+    "sampled_split_prefix": _lib.REDUCE_FORCE_SAMPLED | _lib.REDUCE_SAMPLE_SPLIT | _lib.REDUCE_SAMPLE_PREFIX,
 }
 
 
