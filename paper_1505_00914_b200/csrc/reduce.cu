@@ -634,7 +634,7 @@ __global__ void __launch_bounds__((READ_FIRST && !TMA) ? kThreadsRF : kThreads) 
 
 // ------------------------------------------------------------ sampled
 // Per-column filter built from a sample, exact by construction (mid-size p,
-// DESIGN.md "sampled filter").  Buckets u = (y-1) >> ys with ys chosen so
+// DESIGN.md "sampled filter").  Buckets u = umulhi(y - ybase, qm) with qm chosen so
 // that u <= 254.
 //  1. k_sample_learn: each CTA folds its share of a sample (a prefix of the
 //     input) into a private table of (ua, ub) = (min, max) bucket per column
@@ -682,11 +682,11 @@ __device__ __forceinline__ void sample_init(uint4* smem4, uint32_t wpad, int* __
 // every part of it); on C2 the two measure the same.
 template <bool TMA>
 __device__ __forceinline__ void sample_fold(const int32_t* __restrict__ xy, uint64_t n, uint32_t f256, bool prefix,
-                                            const Geo& g, uint32_t width, uint32_t ys, uint16_t* T, uint8_t* ring,
+                                            const Geo& g, uint32_t width, uint32_t qm, uint16_t* T, uint8_t* ring,
                                             int stages) {
     auto f = [&](int32_t x, int32_t y) {
         const uint32_t s = min(slot_of(x, g.base), width);
-        const uint32_t u = ((uint32_t)y - g.ybase) >> ys;
+        const uint32_t u = __umulhi((uint32_t)y - g.ybase, qm);
         const uint32_t w = T[s];
         const uint32_t nw = min(w & 0xFFu, u) | (max(w >> 8, u) << 8);
         if (nw != w) T[s] = (uint16_t)nw;
@@ -783,7 +783,7 @@ __device__ __forceinline__ uint4 interior_words(const uint4& m, uint32_t chunk, 
 
 template <bool TMA>
 __global__ void __launch_bounds__(kThreads) k_sample_learn(const int32_t* __restrict__ xy, uint64_t n, Geo g,
-                                                           uint32_t width, uint32_t wpad, uint32_t ys,
+                                                           uint32_t width, uint32_t wpad, uint32_t qm,
                                                            uint16_t* __restrict__ scratch, int* __restrict__ DL,
                                                            int init_dl, int stages, uint32_t f256, int prefix) {
     extern __shared__ uint4 smem4[];
@@ -791,7 +791,7 @@ __global__ void __launch_bounds__(kThreads) k_sample_learn(const int32_t* __rest
     pdl_trigger();  // the merge may queue (it cannot co-reside; it waits)
     sample_init(smem4, wpad, DL, width, init_dl);
     __syncthreads();
-    sample_fold<TMA>(xy, n, f256, prefix != 0, g, width, ys, reinterpret_cast<uint16_t*>(smem4), ring, stages);
+    sample_fold<TMA>(xy, n, f256, prefix != 0, g, width, qm, reinterpret_cast<uint16_t*>(smem4), ring, stages);
     __syncthreads();
     sample_dump(smem4, scratch, wpad);
 }
@@ -846,7 +846,7 @@ __device__ __forceinline__ void sts_u16(uint32_t addr, uint32_t v) {
 // shared address tbase (>= width + 1 words; word `width` never skips).
 template <bool TMA>
 __device__ __forceinline__ void sampled_pass(const int32_t* __restrict__ xy, uint64_t n, const Geo& g,
-                                             uint32_t width, uint32_t ys, uint32_t tbase, uint8_t* ring,
+                                             uint32_t width, uint32_t qm, uint32_t tbase, uint8_t* ring,
                                              int stages, int* __restrict__ DL) {
     uint32_t bad = 0;
     // Rare path: a point outside the strict interior of its column.  Inlined
@@ -861,7 +861,7 @@ __device__ __forceinline__ void sampled_pass(const int32_t* __restrict__ xy, uin
         const uint32_t a = tbase + 2 * s;
         const uint32_t w = lds_u16(a);
         const uint32_t lo = w & 0xFFu, span = w >> 8;
-        const uint32_t u = ym1 >> ys;
+        const uint32_t u = __umulhi(ym1, qm);
         if (span == 0) {  // nothing known: both sides may move
             red_min(DL + 2ull * s, y);
             red_min(DL + 2ull * s + 1, ~y);
@@ -878,14 +878,14 @@ __device__ __forceinline__ void sampled_pass(const int32_t* __restrict__ xy, uin
     // Hit test of one point, branch-free: true when it must be settled.  An
     // invalid x clamps to slot `width`, whose word (span 0) never skips (the
     // host guarantees wcheck == width and a table of at least width + 1
-    // slots); an invalid y has (y - 1) >> ys >= every ub of a strict
+    // slots); an invalid y has a bucket >= every ub of a strict
     // interior (or wraps), so it misses too.  Validation thus costs one
     // VIADDMNMX per point instead of two compares, a select and a flag.
     auto test = [&](int32_t x, int32_t y, uint32_t& s) -> bool {
         s = min(slot_of(x, g.base), width);
         const uint32_t w = lds_u16(tbase + 2 * s);
         const uint32_t lo = w & 0xFFu, span = w >> 8;
-        return (((uint32_t)y - g.ybase) >> ys) - lo >= span;  // not strictly inside
+        return __umulhi((uint32_t)y - g.ybase, qm) - lo >= span;  // not strictly inside
     };
     auto one = [&](int32_t x, int32_t y) {
         uint32_t s;
@@ -922,7 +922,7 @@ __device__ __forceinline__ void sampled_pass(const int32_t* __restrict__ xy, uin
 
 template <bool TMA>
 __global__ void __launch_bounds__(kThreads) k_reduce_sampled(const int32_t* __restrict__ xy, uint64_t n, Geo g,
-                                                             uint32_t width, uint32_t wpad, uint32_t ys,
+                                                             uint32_t width, uint32_t wpad, uint32_t qm,
                                                              const uint16_t* __restrict__ F, int stages,
                                                              int* __restrict__ DL) {
     extern __shared__ uint4 smem4[];
@@ -935,7 +935,7 @@ __global__ void __launch_bounds__(kThreads) k_reduce_sampled(const int32_t* __re
         for (uint32_t i = threadIdx.x; i < wpad / 8; i += blockDim.x) smem4[i] = __ldcg(F4 + i);
     }
     __syncthreads();
-    sampled_pass<TMA>(xy, n, g, width, ys, (uint32_t)__cvta_generic_to_shared(smem4), ring, stages, DL);
+    sampled_pass<TMA>(xy, n, g, width, qm, (uint32_t)__cvta_generic_to_shared(smem4), ring, stages, DL);
     if (CHP_PHASE_TIMING) {
         __syncthreads();
         phase_mark(7);
@@ -978,13 +978,13 @@ __device__ __forceinline__ void grid_barrier(GridBar* b) {
 
 // Out of line so phases A-C do not constrain the main pass's registers.
 __device__ __noinline__ void sampled_main_pass(const int32_t* __restrict__ xy, uint64_t n, Geo g, uint32_t width,
-                                               uint32_t ys, uint32_t tbase, int* __restrict__ DL) {
-    sampled_pass<false>(xy, n, g, width, ys, tbase, nullptr, 0, DL);
+                                               uint32_t qm, uint32_t tbase, int* __restrict__ DL) {
+    sampled_pass<false>(xy, n, g, width, qm, tbase, nullptr, 0, DL);
 }
 
 __global__ void __launch_bounds__(kThreads) k_sampled_fused(const int32_t* __restrict__ xy, uint64_t n, uint32_t f256,
                                                             int prefix,
-                                                            Geo g, uint32_t width, uint32_t wpad, uint32_t ys,
+                                                            Geo g, uint32_t width, uint32_t wpad, uint32_t qm,
                                                             uint16_t* __restrict__ scratch, uint16_t* __restrict__ F,
                                                             int* __restrict__ DL, int init_dl, GridBar* bar,
                                                             int merge_only) {
@@ -996,7 +996,7 @@ __global__ void __launch_bounds__(kThreads) k_sampled_fused(const int32_t* __res
     sample_init(smem4, wpad, DL, width, init_dl);
     __syncthreads();
     phase_mark(1);
-    sample_fold<false>(xy, n, f256, prefix != 0, g, width, ys, reinterpret_cast<uint16_t*>(smem4), nullptr, 0);
+    sample_fold<false>(xy, n, f256, prefix != 0, g, width, qm, reinterpret_cast<uint16_t*>(smem4), nullptr, 0);
     __syncthreads();
     phase_mark(2);
     sample_dump(smem4, scratch, wpad);
@@ -1045,7 +1045,7 @@ __global__ void __launch_bounds__(kThreads) k_sampled_fused(const int32_t* __res
     }
     __syncthreads();
     // ---- D: main pass
-    sampled_main_pass(xy, n, g, width, ys, (uint32_t)__cvta_generic_to_shared(smem4), DL);
+    sampled_main_pass(xy, n, g, width, qm, (uint32_t)__cvta_generic_to_shared(smem4), DL);
 }
 
 
@@ -1390,8 +1390,10 @@ int chp_reduce_yr(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t width, 
         case V_SAMPLED: {
             // Sample pass (n/16) -> merged strict-interior table -> one
             // pass over all n points.
-            uint32_t ys = 0;
-            while ((uint64_t)(q - 1) >> ys > 254) ++ys;
+            // Buckets u = umulhi(y - ybase, qm) in [0, 254] over the q valid
+            // values, monotone in y (a shift left power-of-two q at half the
+            // resolution: 2^16 values -> 128 buckets of 512).
+            uint32_t qm = (uint32_t)std::min<uint64_t>(UINT32_MAX, ((uint64_t)255 << 32) / (uint64_t)q);
             const size_t tbytes = (size_t)wpad8 * 2;
             const int sblocks = ctx->sm_count;
             int rc = chp_ensure(ctx, ctx->sample, (size_t)sblocks * tbytes + 16);
@@ -1429,7 +1431,7 @@ int chp_reduce_yr(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t width, 
                     uint16_t* F = (uint16_t*)ctx->filter.p;
                     GridBar* bar = (GridBar*)ctx->gridbar.p;
                     void* args[] = {(void*)&d_xy, (void*)&n, (void*)&f256, (void*)&prefix, (void*)&g, (void*)&w, (void*)&wpad8,
-                                    (void*)&ys,   (void*)&scratch, (void*)&F, (void*)&d_L, (void*)&init, (void*)&bar,
+                                    (void*)&qm,   (void*)&scratch, (void*)&F, (void*)&d_L, (void*)&init, (void*)&bar,
                                     (void*)&merge_only};
                     // (A cooperative launch can be refused when the GPU is
                     // shared and the grid cannot be co-resident: then the
@@ -1447,7 +1449,7 @@ int chp_reduce_yr(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t width, 
                     }
                     const Plan pl = plan_for(ctx, tbytes, flags, false);
                     CHP_LAUNCH_PLANNED_PDL(ctx, pl, k_reduce_sampled<true>, k_reduce_sampled<false>, d_xy, n, g, w,
-                                           wpad8, ys, (const uint16_t*)ctx->filter.p, pl.stages, d_L);
+                                           wpad8, qm, (const uint16_t*)ctx->filter.p, pl.stages, d_L);
                     ctx->variant = "sampled";
                     return CHP_OK;
                 }
@@ -1458,7 +1460,7 @@ int chp_reduce_yr(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t width, 
                 auto fn = sp.tma ? k_sample_learn<true> : k_sample_learn<false>;
                 int unused = 0;
                 if ((rc = kernel_blocks(ctx, (const void*)fn, sp.smem, 1, &unused))) return rc;
-                fn<<<sblocks, kThreads, sp.smem, ctx->stream>>>(d_xy, n, g, w, wpad8, ys, (uint16_t*)ctx->sample.p,
+                fn<<<sblocks, kThreads, sp.smem, ctx->stream>>>(d_xy, n, g, w, wpad8, qm, (uint16_t*)ctx->sample.p,
                                                                 d_L, need_init ? 1 : 0, sp.stages, f256, prefix);
                 CHP_LAUNCHED(ctx);
             }
@@ -1470,7 +1472,7 @@ int chp_reduce_yr(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t width, 
             CHP_LAUNCHED(ctx);
             const Plan pl = plan_for(ctx, tbytes, flags, false);
             CHP_LAUNCH_PLANNED_PDL(ctx, pl, k_reduce_sampled<true>, k_reduce_sampled<false>, d_xy, n, g, w, wpad8,
-                                   ys, (const uint16_t*)ctx->filter.p, pl.stages, d_L);
+                                   qm, (const uint16_t*)ctx->filter.p, pl.stages, d_L);
             ctx->variant = "sampled";
             return CHP_OK;
         }
