@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--n", type=int, default=0, help="override points per rank (default: the config's n)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--flags", type=int, default=0, help="chp_reduce flags (variant forcing, experiments)")
+    ap.add_argument("--q-unset", action="store_true",
+                    help="K1 without the y bound q (the reference API's default; not the headline)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
@@ -249,7 +251,7 @@ def main():
         if mode:
             a = torch.cuda.Event(enable_timing=True)
             a.record(stream)
-        ctx.reduce(xy, p, q=p, out=DL, flags=args.flags)
+        ctx.reduce(xy, p, q=None if args.q_unset else p, out=DL, flags=args.flags)
         if mode == "k1":
             b = torch.cuda.Event(enable_timing=True)
             b.record(stream)

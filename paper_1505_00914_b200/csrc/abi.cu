@@ -642,7 +642,7 @@ void chp_ctx_destroy(chp_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     cudaStreamSynchronize(ctx->copy_stream);
     DevBuf* bufs[] = {&ctx->tile_status, &ctx->hull_a, &ctx->hull_b, &ctx->hull_cnt_a, &ctx->hull_cnt_b,
-                      &ctx->filter, &ctx->sample, &ctx->gridbar, &ctx->dl, &ctx->counts, &ctx->chain, &ctx->lower, &ctx->upper,
+                      &ctx->filter, &ctx->sample, &ctx->gridbar, &ctx->yrange, &ctx->dl, &ctx->counts, &ctx->chain, &ctx->lower, &ctx->upper,
                       &ctx->hull, &ctx->occ, &ctx->lpairs, &ctx->stage_dev[0], &ctx->stage_dev[1]};
     for (DevBuf* b : bufs) free_buf(*b);
     free_buf(ctx->unpack_dev[0]);

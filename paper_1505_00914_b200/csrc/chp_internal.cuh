@@ -38,6 +38,7 @@ struct chp_ctx {
     DevBuf filter;       // K1 filter snapshot
     DevBuf sample;       // K1 sampled filter: per-CTA learned tables
     DevBuf gridbar;      // grid barrier of the cooperative sampled kernel
+    DevBuf yrange;       // K1 sampled filter, q unset: per-CTA y range of a prefix
     int coop = 0;        // cudaDevAttrCooperativeLaunch
     DevBuf dl;           // host pipeline: device-form L
     DevBuf counts;       // host pipeline: int64[8]

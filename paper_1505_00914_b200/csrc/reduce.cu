@@ -634,7 +634,7 @@ __global__ void __launch_bounds__((READ_FIRST && !TMA) ? kThreadsRF : kThreads) 
 
 // ------------------------------------------------------------ sampled
 // Per-column filter built from a sample, exact by construction (mid-size p,
-// DESIGN.md "sampled filter").  Buckets u = umulhi(y - ybase, qm) with qm chosen so
+// DESIGN.md "sampled filter").  Buckets u = umulhi(y - base, m) (Quant) chosen so
 // that u <= 254.
 //  1. k_sample_learn: each CTA folds its share of a sample (a prefix of the
 //     input) into a private table of (ua, ub) = (min, max) bucket per column
@@ -653,6 +653,89 @@ __global__ void __launch_bounds__((READ_FIRST && !TMA) ? kThreadsRF : kThreads) 
 // Tables are dumped as (ua, 255 - ub) so the merge is one byte-wise min.
 // With init_dl the kernel also initialises DL (the main pass runs after it in
 // stream order), saving the separate k_dl_init launch.
+// Quantisation of y into the table's buckets: u = umulhi(y - base, m), in
+// [0, 254] over the range the table covers.  With q known the range is the
+// valid range (base = ybase); with q unset (validation only y >= ybase) it is
+// speculative, [min, max] of the valid y in a 2^18-point prefix (k_yrange, one partial
+// per CTA, reduced by every consumer CTA): a point outside it is still exact,
+// it folds into the edge bucket and always misses the main-pass test (below
+// the base its offset wraps past every bucket), and settle moves the side it
+// lies on.
+struct Quant {
+    int32_t base;
+    uint32_t m;
+};
+
+__host__ __device__ inline uint32_t quant_mult(uint64_t count) {
+    const uint64_t m = ((uint64_t)255 << 32) / (count ? count : 1);
+    return m > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)m;
+}
+
+// One round trip: a 2^18-point prefix over 148 x 1024 threads.
+__global__ void __launch_bounds__(1024) k_yrange(const int32_t* __restrict__ xy, uint64_t n, Geo g,
+                                                 int2* __restrict__ part) {
+    __shared__ int2 red[32];
+    int lo = INT_MAX, hi = INT_MIN;
+    auto f = [&](int32_t x, int32_t y) {
+        uint32_t s;
+        if (accept<true>(g, x, y, s)) {
+            lo = min(lo, y);
+            hi = max(hi, y);
+        }
+    };
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const int2 p = reinterpret_cast<const int2*>(xy)[i];
+        f(p.x, p.y);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = make_int2(lo, hi);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int k = 1; k < (int)(blockDim.x >> 5); ++k) {
+            lo = min(lo, red[k].x);
+            hi = max(hi, red[k].y);
+        }
+        part[blockIdx.x] = make_int2(lo, hi);
+    }
+}
+
+// Every CTA derives the same Quant from the k_yrange partials (warp 0
+// reduces them; the result is broadcast through shared memory).
+__device__ __forceinline__ Quant resolve_quant(Quant qz, const int2* __restrict__ part, uint32_t np, const Geo& g) {
+    if (!part) return qz;
+    __shared__ Quant s_q;
+    if (threadIdx.x < 32) {
+        int lo = INT_MAX, hi = INT_MIN;
+        for (uint32_t i = threadIdx.x; i < np; i += 32) {
+            const int2 v = __ldcg(part + i);
+            lo = min(lo, v.x);
+            hi = max(hi, v.y);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        }
+        if (threadIdx.x == 0) {
+            Quant r;
+            if (lo > hi) {  // no valid y in the prefix: the whole valid range
+                r.base = (int32_t)g.ybase;
+                r.m = quant_mult(g.qmax);
+            } else {
+                r.base = lo;
+                r.m = quant_mult((uint64_t)((int64_t)hi - lo + 1));
+            }
+            s_q = r;
+        }
+    }
+    __syncthreads();
+    return s_q;
+}
+
 // Phase helpers shared by the three-launch pipeline and the fused kernel.
 __device__ __forceinline__ void sample_init(uint4* smem4, uint32_t wpad, int* __restrict__ DL, uint32_t width,
                                             int init_dl) {
@@ -680,13 +763,17 @@ __device__ __forceinline__ void sample_init(uint4* smem4, uint32_t wpad, int* __
 // take the first n * f256 / 256 points instead.  The heads spread the sample
 // over the whole input (an input sorted by x or y still yields a table for
 // every part of it); on C2 the two measure the same.
-template <bool TMA>
+template <bool TMA, bool SPEC>
 __device__ __forceinline__ void sample_fold(const int32_t* __restrict__ xy, uint64_t n, uint32_t f256, bool prefix,
-                                            const Geo& g, uint32_t width, uint32_t qm, uint16_t* T, uint8_t* ring,
+                                            const Geo& g, uint32_t width, Quant qz, uint16_t* T, uint8_t* ring,
                                             int stages) {
     auto f = [&](int32_t x, int32_t y) {
         const uint32_t s = min(slot_of(x, g.base), width);
-        const uint32_t u = __umulhi((uint32_t)y - g.ybase, qm);
+        // Outside the quantised range: the edge bucket (0 or 254).
+        // (q known: every valid y is in range; an invalid one may garble its
+        // own column's word, and the main pass fails the call.)
+        const uint32_t uq = __umulhi((uint32_t)y - (uint32_t)qz.base, qz.m);
+        const uint32_t u = SPEC ? (y < qz.base ? 0u : min(uq, 254u)) : uq;
         const uint32_t w = T[s];
         const uint32_t nw = min(w & 0xFFu, u) | (max(w >> 8, u) << 8);
         if (nw != w) T[s] = (uint16_t)nw;
@@ -781,17 +868,19 @@ __device__ __forceinline__ uint4 interior_words(const uint4& m, uint32_t chunk, 
     return make_uint4(out[0], out[1], out[2], out[3]);
 }
 
-template <bool TMA>
+template <bool TMA, bool SPEC>
 __global__ void __launch_bounds__(kThreads) k_sample_learn(const int32_t* __restrict__ xy, uint64_t n, Geo g,
-                                                           uint32_t width, uint32_t wpad, uint32_t qm,
+                                                           uint32_t width, uint32_t wpad, Quant qz,
+                                                           const int2* __restrict__ qpart, uint32_t nqpart,
                                                            uint16_t* __restrict__ scratch, int* __restrict__ DL,
                                                            int init_dl, int stages, uint32_t f256, int prefix) {
     extern __shared__ uint4 smem4[];
     uint8_t* ring = reinterpret_cast<uint8_t*>(smem4) + table_span((size_t)wpad * 2);
     pdl_trigger();  // the merge may queue (it cannot co-reside; it waits)
+    if (SPEC) qz = resolve_quant(qz, qpart, nqpart, g);
     sample_init(smem4, wpad, DL, width, init_dl);
     __syncthreads();
-    sample_fold<TMA>(xy, n, f256, prefix != 0, g, width, qm, reinterpret_cast<uint16_t*>(smem4), ring, stages);
+    sample_fold<TMA, SPEC>(xy, n, f256, prefix != 0, g, width, qz, reinterpret_cast<uint16_t*>(smem4), ring, stages);
     __syncthreads();
     sample_dump(smem4, scratch, wpad);
 }
@@ -844,9 +933,9 @@ __device__ __forceinline__ void sts_u16(uint32_t addr, uint32_t v) {
 
 // The main pass over all n points against the strict-interior table at
 // shared address tbase (>= width + 1 words; word `width` never skips).
-template <bool TMA>
+template <bool TMA, bool SPEC>
 __device__ __forceinline__ void sampled_pass(const int32_t* __restrict__ xy, uint64_t n, const Geo& g,
-                                             uint32_t width, uint32_t qm, uint32_t tbase, uint8_t* ring,
+                                             uint32_t width, Quant qz, uint32_t tbase, uint8_t* ring,
                                              int stages, int* __restrict__ DL) {
     uint32_t bad = 0;
     // Rare path: a point outside the strict interior of its column.  Inlined
@@ -861,15 +950,21 @@ __device__ __forceinline__ void sampled_pass(const int32_t* __restrict__ xy, uin
         const uint32_t a = tbase + 2 * s;
         const uint32_t w = lds_u16(a);
         const uint32_t lo = w & 0xFFu, span = w >> 8;
-        const uint32_t u = __umulhi(ym1, qm);
         if (span == 0) {  // nothing known: both sides may move
             red_min(DL + 2ull * s, y);
             red_min(DL + 2ull * s + 1, ~y);
             return;
         }
-        if (u < lo) {  // at/below the lower boundary bucket: only lo moves
+        // SPEC (q unset): below the quantised range counts as bucket -1,
+        // above it as bucket 255 (past every stored bucket).  Otherwise every
+        // valid y is in range.
+        const bool below = SPEC && y < qz.base;
+        const uint32_t uq = __umulhi((uint32_t)y - (uint32_t)qz.base, qz.m);
+        const uint32_t u = SPEC ? (below ? 0u : min(uq, 255u)) : uq;
+        if (below || u < lo) {  // at/below the lower boundary bucket: only lo moves
             red_min(DL + 2ull * s, y);
-            if (u + 1 < lo) sts_u16(a, (u + 1) | ((lo + span - u - 1) << 8));
+            const uint32_t nlo = below ? 0u : u + 1;
+            if (nlo < lo) sts_u16(a, nlo | ((lo + span - nlo) << 8));
         } else if (u >= lo + span) {  // at/above the upper boundary bucket: only hi moves
             red_min(DL + 2ull * s + 1, ~y);
             if (u > lo + span) sts_u16(a, lo | ((u - lo) << 8));
@@ -885,7 +980,7 @@ __device__ __forceinline__ void sampled_pass(const int32_t* __restrict__ xy, uin
         s = min(slot_of(x, g.base), width);
         const uint32_t w = lds_u16(tbase + 2 * s);
         const uint32_t lo = w & 0xFFu, span = w >> 8;
-        return __umulhi((uint32_t)y - g.ybase, qm) - lo >= span;  // not strictly inside
+        return __umulhi((uint32_t)y - (uint32_t)qz.base, qz.m) - lo >= span;  // not strictly inside
     };
     auto one = [&](int32_t x, int32_t y) {
         uint32_t s;
@@ -920,9 +1015,10 @@ __device__ __forceinline__ void sampled_pass(const int32_t* __restrict__ xy, uin
     flag_error(bad != 0, DL, width);
 }
 
-template <bool TMA>
+template <bool TMA, bool SPEC>
 __global__ void __launch_bounds__(kThreads) k_reduce_sampled(const int32_t* __restrict__ xy, uint64_t n, Geo g,
-                                                             uint32_t width, uint32_t wpad, uint32_t qm,
+                                                             uint32_t width, uint32_t wpad, Quant qz,
+                                                             const int2* __restrict__ qpart, uint32_t nqpart,
                                                              const uint16_t* __restrict__ F, int stages,
                                                              int* __restrict__ DL) {
     extern __shared__ uint4 smem4[];
@@ -930,12 +1026,13 @@ __global__ void __launch_bounds__(kThreads) k_reduce_sampled(const int32_t* __re
     pdl_trigger();
     pdl_wait();  // the merged table (and DL, initialised by the sample pass)
     phase_mark(6);
+    if (SPEC) qz = resolve_quant(qz, qpart, nqpart, g);
     {
         const uint4* F4 = reinterpret_cast<const uint4*>(F);
         for (uint32_t i = threadIdx.x; i < wpad / 8; i += blockDim.x) smem4[i] = __ldcg(F4 + i);
     }
     __syncthreads();
-    sampled_pass<TMA>(xy, n, g, width, qm, (uint32_t)__cvta_generic_to_shared(smem4), ring, stages, DL);
+    sampled_pass<TMA, SPEC>(xy, n, g, width, qz, (uint32_t)__cvta_generic_to_shared(smem4), ring, stages, DL);
     if (CHP_PHASE_TIMING) {
         __syncthreads();
         phase_mark(7);
@@ -978,13 +1075,15 @@ __device__ __forceinline__ void grid_barrier(GridBar* b) {
 
 // Out of line so phases A-C do not constrain the main pass's registers.
 __device__ __noinline__ void sampled_main_pass(const int32_t* __restrict__ xy, uint64_t n, Geo g, uint32_t width,
-                                               uint32_t qm, uint32_t tbase, int* __restrict__ DL) {
-    sampled_pass<false>(xy, n, g, width, qm, tbase, nullptr, 0, DL);
+                                               Quant qz, uint32_t tbase, int* __restrict__ DL) {
+    sampled_pass<false, true>(xy, n, g, width, qz, tbase, nullptr, 0, DL);
 }
 
+template <bool SPEC>
 __global__ void __launch_bounds__(kThreads) k_sampled_fused(const int32_t* __restrict__ xy, uint64_t n, uint32_t f256,
                                                             int prefix,
-                                                            Geo g, uint32_t width, uint32_t wpad, uint32_t qm,
+                                                            Geo g, uint32_t width, uint32_t wpad, Quant qz,
+                                                            const int2* __restrict__ qpart, uint32_t nqpart,
                                                             uint16_t* __restrict__ scratch, uint16_t* __restrict__ F,
                                                             int* __restrict__ DL, int init_dl, GridBar* bar,
                                                             int merge_only) {
@@ -992,11 +1091,12 @@ __global__ void __launch_bounds__(kThreads) k_sampled_fused(const int32_t* __res
     const uint32_t nchunks = wpad / 8;
     if (merge_only) pdl_trigger();  // the main pass (a dependent launch) may queue
     phase_mark(0);
+    if (SPEC) qz = resolve_quant(qz, qpart, nqpart, g);
     // ---- A: sample pass + DL init
     sample_init(smem4, wpad, DL, width, init_dl);
     __syncthreads();
     phase_mark(1);
-    sample_fold<false>(xy, n, f256, prefix != 0, g, width, qm, reinterpret_cast<uint16_t*>(smem4), nullptr, 0);
+    sample_fold<false, SPEC>(xy, n, f256, prefix != 0, g, width, qz, reinterpret_cast<uint16_t*>(smem4), nullptr, 0);
     __syncthreads();
     phase_mark(2);
     sample_dump(smem4, scratch, wpad);
@@ -1045,7 +1145,7 @@ __global__ void __launch_bounds__(kThreads) k_sampled_fused(const int32_t* __res
     }
     __syncthreads();
     // ---- D: main pass
-    sampled_main_pass(xy, n, g, width, qm, (uint32_t)__cvta_generic_to_shared(smem4), DL);
+    sampled_main_pass(xy, n, g, width, qz, (uint32_t)__cvta_generic_to_shared(smem4), DL);
 }
 
 
@@ -1313,7 +1413,10 @@ int chp_reduce_yr(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t width, 
     const bool fits_f8 = yknown && ybase == 1 && (size_t)((w + 7) & ~7u) * 2 <= budget;  // quant8 assumes y >= 1
 
     const uint32_t wpad8 = (w + 8) & ~7u;  // >= w + 1: slot w is the invalid-x sink
-    const bool fits_sampled = yknown && g.wcheck == w && (size_t)wpad8 * 2 <= budget;
+    // q unset (validation y >= ybase only): the sampled filter quantises a
+    // speculative range from a prefix instead (Quant, k_yrange).
+    const bool yspec = validate && q < 0 && ybase >= 0;
+    const bool fits_sampled = (yknown || yspec) && g.wcheck == w && (size_t)wpad8 * 2 <= budget;
     const bool fits_filter = yknown && g.wcheck == w;  // invalid x must clamp onto the sink
 
     enum { V_GLOBAL, V_SMEM32, V_SMEM16, V_FILTER8, V_FILTER, V_SAMPLED } v;
@@ -1390,10 +1493,23 @@ int chp_reduce_yr(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t width, 
         case V_SAMPLED: {
             // Sample pass (n/16) -> merged strict-interior table -> one
             // pass over all n points.
-            // Buckets u = umulhi(y - ybase, qm) in [0, 254] over the q valid
+            // Buckets u = umulhi(y - base, m) in [0, 254] over the q valid
             // values, monotone in y (a shift left power-of-two q at half the
-            // resolution: 2^16 values -> 128 buckets of 512).
-            uint32_t qm = (uint32_t)std::min<uint64_t>(UINT32_MAX, ((uint64_t)255 << 32) / (uint64_t)q);
+            // resolution: 2^16 values -> 128 buckets of 512).  q unset: the
+            // range of the valid y in the first 2^18 points, resolved on the
+            // device by every consumer CTA from k_yrange's partials.
+            Quant qz{(int32_t)g.ybase, yknown ? quant_mult((uint64_t)q) : quant_mult(g.qmax)};
+            const int2* qpart = nullptr;
+            uint32_t nqpart = 0;
+            if (!yknown) {
+                nqpart = (uint32_t)ctx->sm_count;
+                int rc0 = chp_ensure(ctx, ctx->yrange, (size_t)nqpart * sizeof(int2));
+                if (rc0) return rc0;
+                qpart = (const int2*)ctx->yrange.p;
+                k_yrange<<<nqpart, 1024, 0, ctx->stream>>>(d_xy, std::min<uint64_t>(n, 1ull << 18), g,
+                                                            (int2*)ctx->yrange.p);
+                CHP_LAUNCHED(ctx);
+            }
             const size_t tbytes = (size_t)wpad8 * 2;
             const int sblocks = ctx->sm_count;
             int rc = chp_ensure(ctx, ctx->sample, (size_t)sblocks * tbytes + 16);
@@ -1421,22 +1537,23 @@ int chp_reduce_yr(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t width, 
                     CHP_CUDA(ctx, cudaMemsetAsync(ctx->gridbar.p, 0, 64, ctx->stream));
                 }
                 const size_t smem = std::max(table_span(tbytes), kFusedMergeSmem);
-                CHP_CUDA(ctx, cudaFuncSetAttribute(k_sampled_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                const void* fused = yknown ? (const void*)k_sampled_fused<false> : (const void*)k_sampled_fused<true>;
+                CHP_CUDA(ctx, cudaFuncSetAttribute(fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    (int)smem));
                 int per_sm = 0;
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sampled_fused, kThreads, smem);
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused, kThreads, smem);
                 if (per_sm >= 1) {
                     const int init = need_init ? 1 : 0;
                     uint16_t* scratch = (uint16_t*)ctx->sample.p;
                     uint16_t* F = (uint16_t*)ctx->filter.p;
                     GridBar* bar = (GridBar*)ctx->gridbar.p;
                     void* args[] = {(void*)&d_xy, (void*)&n, (void*)&f256, (void*)&prefix, (void*)&g, (void*)&w, (void*)&wpad8,
-                                    (void*)&qm,   (void*)&scratch, (void*)&F, (void*)&d_L, (void*)&init, (void*)&bar,
+                                    (void*)&qz, (void*)&qpart, (void*)&nqpart, (void*)&scratch, (void*)&F, (void*)&d_L, (void*)&init, (void*)&bar,
                                     (void*)&merge_only};
                     // (A cooperative launch can be refused when the GPU is
                     // shared and the grid cannot be co-resident: then the
                     // split form below runs instead.)
-                    const cudaError_t ce = cudaLaunchCooperativeKernel((const void*)k_sampled_fused, dim3(sblocks),
+                    const cudaError_t ce = cudaLaunchCooperativeKernel(fused, dim3(sblocks),
                                                                        dim3(kThreads), args, smem, ctx->stream);
                     if (ce != cudaSuccess) {
                         cudaGetLastError();
@@ -1444,23 +1561,31 @@ int chp_reduce_yr(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t width, 
                     }
                     CHP_LAUNCHED(ctx);
                     if (!merge_only) {
-                        ctx->variant = "sampled-fused";
+                        ctx->variant = yknown ? "sampled-fused" : "sampled-fused-yspec";
                         return CHP_OK;
                     }
                     const Plan pl = plan_for(ctx, tbytes, flags, false);
-                    CHP_LAUNCH_PLANNED_PDL(ctx, pl, k_reduce_sampled<true>, k_reduce_sampled<false>, d_xy, n, g, w,
-                                           wpad8, qm, (const uint16_t*)ctx->filter.p, pl.stages, d_L);
-                    ctx->variant = "sampled";
+                    if (yknown)
+                        CHP_LAUNCH_PLANNED_PDL(ctx, pl, (k_reduce_sampled<true, false>),
+                                               (k_reduce_sampled<false, false>), d_xy, n, g, w, wpad8, qz, qpart,
+                                               nqpart, (const uint16_t*)ctx->filter.p, pl.stages, d_L);
+                    else
+                        CHP_LAUNCH_PLANNED_PDL(ctx, pl, (k_reduce_sampled<true, true>), (k_reduce_sampled<false, true>),
+                                               d_xy, n, g, w, wpad8, qz, qpart, nqpart,
+                                               (const uint16_t*)ctx->filter.p, pl.stages, d_L);
+                    ctx->variant = yknown ? "sampled" : "sampled-yspec";
                     return CHP_OK;
                 }
             }
         split:
             {
                 const Plan sp = plan_for(ctx, tbytes, (flags & CHP_REDUCE_SAMPLE_TMA) ? CHP_REDUCE_TMA : 0u, false);
-                auto fn = sp.tma ? k_sample_learn<true> : k_sample_learn<false>;
+                auto fn = sp.tma ? (yknown ? k_sample_learn<true, false> : k_sample_learn<true, true>)
+                                 : (yknown ? k_sample_learn<false, false> : k_sample_learn<false, true>);
                 int unused = 0;
                 if ((rc = kernel_blocks(ctx, (const void*)fn, sp.smem, 1, &unused))) return rc;
-                fn<<<sblocks, kThreads, sp.smem, ctx->stream>>>(d_xy, n, g, w, wpad8, qm, (uint16_t*)ctx->sample.p,
+                fn<<<sblocks, kThreads, sp.smem, ctx->stream>>>(d_xy, n, g, w, wpad8, qz, qpart, nqpart,
+                                                                (uint16_t*)ctx->sample.p,
                                                                 d_L, need_init ? 1 : 0, sp.stages, f256, prefix);
                 CHP_LAUNCHED(ctx);
             }
@@ -1471,9 +1596,15 @@ int chp_reduce_yr(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t width, 
                                      (uint16_t*)ctx->filter.p));
             CHP_LAUNCHED(ctx);
             const Plan pl = plan_for(ctx, tbytes, flags, false);
-            CHP_LAUNCH_PLANNED_PDL(ctx, pl, k_reduce_sampled<true>, k_reduce_sampled<false>, d_xy, n, g, w, wpad8,
-                                   qm, (const uint16_t*)ctx->filter.p, pl.stages, d_L);
-            ctx->variant = "sampled";
+            if (yknown)
+                CHP_LAUNCH_PLANNED_PDL(ctx, pl, (k_reduce_sampled<true, false>), (k_reduce_sampled<false, false>), d_xy,
+                                       n, g, w, wpad8, qz, qpart, nqpart, (const uint16_t*)ctx->filter.p, pl.stages,
+                                       d_L);
+            else
+                CHP_LAUNCH_PLANNED_PDL(ctx, pl, (k_reduce_sampled<true, true>), (k_reduce_sampled<false, true>), d_xy,
+                                       n, g, w, wpad8, qz, qpart, nqpart, (const uint16_t*)ctx->filter.p, pl.stages,
+                                       d_L);
+            ctx->variant = yknown ? "sampled" : "sampled-yspec";
             return CHP_OK;
         }
         case V_FILTER: {

@@ -157,6 +157,33 @@ def test_large_y_without_q(ctx, orc):
         check_against_oracle(orc, got, xy, 3, None)
 
 
+@pytest.mark.parametrize("case", ["narrow_prefix", "sorted_desc", "gaussian"])
+def test_q_unset_speculative_range(ctx, orc, case):
+    """q unset with a width beyond the smem tables: the sampled filter
+    quantises the y range of the first 2^18 points; points outside it (both
+    sides, far) must still be exact, and an invalid y must still fail."""
+    rng = np.random.default_rng(77)
+    p, n = 65536, 3_000_000
+    x = rng.integers(1, p + 1, size=n)
+    if case == "narrow_prefix":
+        y = rng.integers(1000, 2000, size=n)
+        tail = np.arange(n) >= (1 << 18)
+        y[tail] = rng.integers(1, 2147483647, size=int(tail.sum()))
+    elif case == "sorted_desc":
+        y = np.sort(rng.integers(1, 1 << 30, size=n))[::-1].copy()
+    else:
+        y = np.clip(np.rint(rng.normal(p / 2, p / 8, size=n)), 1, p)
+    xy = np.stack([x, y], axis=1).astype(np.int32)
+    got = run_device(ctx, xy, p, None)
+    assert ctx.variant.startswith("sampled") and ctx.variant.endswith("yspec"), ctx.variant
+    check_against_oracle(orc, got, xy, p, None)
+    bad = xy.copy()
+    bad[n - 5] = (7, 0)
+    DL = ctx.reduce(torch.from_numpy(bad).cuda(), p)
+    with pytest.raises(ValueError):
+        ctx.check(DL, p)
+
+
 def test_randomized_fixtures(ctx, orc):
     rng = np.random.default_rng(2026)
     for trial in range(300):
