@@ -40,6 +40,7 @@ struct chp_ctx {
     DevBuf gridbar;      // grid barrier of the cooperative sampled kernel
     DevBuf yrange;       // K1 sampled filter, q unset: per-CTA y range of a prefix
     int coop = 0;        // cudaDevAttrCooperativeLaunch
+    int hull_coop_checked = 0, hull_coop_ok = 0, hull_leaf_attr = 0;  // K4 launch shape (hull.cu)
     DevBuf dl;           // host pipeline: device-form L
     DevBuf counts;       // host pipeline: int64[8]
     DevBuf chain, lower, upper, hull, occ, lpairs;
@@ -128,6 +129,33 @@ __device__ __forceinline__ int4 ld_stream(const int4* p) {
                  : "l"(p));
     return r;
 }
+// Grid-wide barrier of a cooperative launch (every CTA co-resident).
+struct GridBar {
+    unsigned long long count;  // arrivals since the context was created (see grid_barrier)
+};
+
+__device__ __forceinline__ void grid_barrier(GridBar* b) {
+    // One atomic per CTA and no reset: arrival k of barrier round r sees
+    // old = r * G + k, and the round is complete once the 64-bit counter
+    // reaches (r + 1) * G.  Every cooperative launch on a context uses the
+    // same grid size G (one CTA per SM).  The last arrival's add releases
+    // everyone directly (the reset-and-flip form needed two more serialised
+    // L2 round trips, ~2 us at 148 CTAs).
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned long long G = gridDim.x;
+        const unsigned long long old = atomicAdd(&b->count, 1ull);
+        const unsigned long long target = old - old % G + G;
+        unsigned long long cur;
+        do {
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(cur) : "l"(&b->count) : "memory");
+        } while (cur < target);
+        __threadfence();
+    }
+    __syncthreads();
+}
+
 // L2-coherent load of a slot pair that other CTAs update atomically.
 __device__ __forceinline__ int2 ld_cg2(const int2* p) {
     int2 r;

@@ -22,13 +22,16 @@
 //            with B[j+1] strictly above line q -> B[j] (binary search per
 //            lane; the rightmost touching point, so collinear bridge points
 //            drop out).  Result A[0..i*] ++ B[t*..].
-//   final  : one thread stitches lower ++ upper (dropping the shared end
+//   final  : one CTA stitches lower ++ upper (dropping the shared end
 //            points of single-point extreme columns), which is already CCW
 //            from the lexicographic minimum; degenerate sets come out as
 //            1 or 2 vertices {lexmin, lexmax} as in src/geometry.cpp:394-403.
+// With cooperative launch the three stages are ONE kernel (a grid barrier
+// per merge level); otherwise one launch per stage and level.
 // Orientation tests are exact (__int128 cross products,
 // include/chp/geometry.hpp:29-35).
 #include <algorithm>
+#include <cstdlib>
 
 #include "chp_internal.cuh"
 
@@ -59,27 +62,30 @@ __device__ __forceinline__ P seq_point(const int2* lower, const int2* upper, lon
     return P{-(long long)q.x, -(long long)q.y};
 }
 
-__global__ void k_hull_leaf(const int2* __restrict__ lower, const int2* __restrict__ upper,
-                            const long long* __restrict__ counts, uint32_t nchunks, uint64_t cap,
-                            P* __restrict__ buf, int* __restrict__ cnt) {
-    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
-    const int prob = blockIdx.y;
-    if (c >= nchunks) return;
-    const long long v = counts[1];
+// Chunk c of problem `prob`: the strict monotone chain over its <= 32
+// points, with the stack in shared memory (a global-memory stack put a
+// store->load round trip in every step: 48-54 us at C2/C3).
+__device__ __forceinline__ void leaf_chunk(const int2* __restrict__ lower, const int2* __restrict__ upper, long long v,
+                                           int prob, uint32_t c, uint32_t nchunks, uint64_t cap, P* stack,
+                                           P* __restrict__ buf, int* __restrict__ cnt) {
     const long long b = (long long)c * kLeaf;
     int* cp = cnt + (size_t)prob * nchunks + c;
     if (b >= v) {
         *cp = 0;
         return;
     }
-    const long long e = min(b + kLeaf, v);
-    P* out = buf + (size_t)prob * cap + b;
+    const int m = (int)(min(b + kLeaf, v) - b);
+    // All loads first (in flight together), then the chain in place: the
+    // stack top k never passes the read position i.
+    for (int i = 0; i < m; ++i) stack[i] = seq_point(lower, upper, v, prob, b + i);
     int k = 0;
-    for (long long i = b; i < e; ++i) {
-        const P q = seq_point(lower, upper, v, prob, i);
-        while (k >= 2 && orient(out[k - 2], out[k - 1], q) <= 0) --k;
-        out[k++] = q;
+    for (int i = 0; i < m; ++i) {
+        const P q = stack[i];
+        while (k >= 2 && orient(stack[k - 2], stack[k - 1], q) <= 0) --k;
+        stack[k++] = q;
     }
+    P* out = buf + (size_t)prob * cap + b;
+    for (int i = 0; i < k; ++i) out[i] = stack[i];
     *cp = k;
 }
 
@@ -96,13 +102,17 @@ __device__ __forceinline__ int tangent(const P& q, const P* B, int nb) {
     return lo;
 }
 
-__global__ void k_hull_merge(const P* __restrict__ in, const int* __restrict__ cnt_in, P* __restrict__ out,
-                             int* __restrict__ cnt_out, uint32_t nchunks, uint64_t cap, uint32_t nregions,
-                             uint64_t region_cap) {
-    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
+// Warp gw (< 2 * npairs, warp-uniform) merges regions 2m and 2m+1 of its
+// problem.
+// Hulls of up to kStage points in total are first staged in the warp's
+// shared-memory slab `wsm` (one coalesced round trip), so the searches'
+// dependent loads hit shared memory instead of L2.
+constexpr int kStage = 256;
+__device__ __forceinline__ void merge_pair(uint32_t gw, int lane, const P* __restrict__ in,
+                                           const int* __restrict__ cnt_in, P* __restrict__ out,
+                                           int* __restrict__ cnt_out, uint32_t nchunks, uint64_t cap,
+                                           uint32_t nregions, uint64_t region_cap, P* wsm) {
     const uint32_t npairs = (nregions + 1) / 2;
-    if (gw >= 2 * npairs) return;
     const int prob = gw / npairs;
     const uint32_t m = gw % npairs;
     const uint32_t ra = 2 * m, rb = 2 * m + 1;
@@ -118,6 +128,13 @@ __global__ void k_hull_merge(const P* __restrict__ in, const int* __restrict__ c
         for (int k = lane; k < ns; k += 32) O[k] = src[k];
         if (lane == 0) *co = ns;
         return;
+    }
+    if (wsm && na + nb <= kStage) {
+        for (int k = lane; k < na; k += 32) wsm[k] = A[k];
+        for (int k = lane; k < nb; k += 32) wsm[na + k] = B[k];
+        __syncwarp();
+        A = wsm;
+        B = wsm + na;
     }
     // i* = first i in [0, na-1] with Q(i) false; Q(na-1) = false.
     int lo = 0, hi = na - 1;
@@ -154,45 +171,139 @@ __global__ void k_hull_merge(const P* __restrict__ in, const int* __restrict__ c
     for (int k = lane; k < keep_a; k += 32) O[k] = A[k];
     for (int k = tstar + lane; k < nb; k += 32) O[keep_a + (k - tstar)] = B[k];
     if (lane == 0) *co = keep_a + (nb - tstar);
+    __syncwarp();  // the slab is reused by the warp's next pair
 }
 
-__global__ void k_hull_final(const P* __restrict__ fin, const int* __restrict__ cnt_fin, uint32_t nchunks,
-                             uint64_t cap, const long long* __restrict__ counts, int swapped,
-                             P* __restrict__ tmp, int2* __restrict__ hull, long long* __restrict__ h_out) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// The whole CTA: lower ++ reflected upper (dropping the shared end points of
+// single-point extreme columns), the axis swap (a reflection, so the order
+// reverses for h >= 3), then the rotation to the lexicographic minimum.
+// (One thread with a 64-bit modulo per vertex took 314 us at h = 1066.)
+__device__ __forceinline__ void final_block(const P* __restrict__ fin, const int* __restrict__ cnt_fin,
+                                            uint32_t nchunks, uint64_t cap, const long long* __restrict__ counts,
+                                            int swapped, P* __restrict__ tmp, int2* __restrict__ hull,
+                                            long long* __restrict__ h_out) {
+    __shared__ long long s_best[32];
     if (counts[1] == 0) {
-        *h_out = 0;
+        if (threadIdx.x == 0) *h_out = 0;
         return;
     }
     const P* HL = fin;
     const int nl = cnt_fin[0];
     const P* HU = fin + cap;
     const int nu = cnt_fin[nchunks];
-    long long h = 0;
-    for (int k = 0; k < nl; ++k) tmp[h++] = HL[k];
     const P u0{-HU[0].x, -HU[0].y};
     const P ul{-HU[nu - 1].x, -HU[nu - 1].y};
     const int st = peq(u0, HL[nl - 1]) ? 1 : 0;
     const int en = peq(ul, HL[0]) ? nu - 1 : nu;
-    for (int k = st; k < en; ++k) tmp[h++] = P{-HU[k].x, -HU[k].y};
-    if (swapped) {
-        for (long long k = 0; k < h; ++k) tmp[k] = P{tmp[k].y, tmp[k].x};
-        if (h >= 3) {  // a reflection flips the orientation
-            for (long long i = 0, j = h - 1; i < j; ++i, --j) {
-                const P t = tmp[i];
-                tmp[i] = tmp[j];
-                tmp[j] = t;
-            }
-        }
+    const long long h = nl + (long long)(en > st ? en - st : 0);  // (one point: st = 1 > en = 0)
+    const bool rev = swapped && h >= 3;
+    for (long long k = threadIdx.x; k < h; k += blockDim.x) {
+        P q = k < nl ? HL[k] : P{-HU[st + (k - nl)].x, -HU[st + (k - nl)].y};
+        if (swapped) q = P{q.y, q.x};
+        tmp[rev ? h - 1 - k : k] = q;
     }
-    long long start = 0;
-    for (long long k = 1; k < h; ++k)
-        if (lex_less(tmp[k], tmp[start])) start = k;
-    for (long long k = 0; k < h; ++k) {
-        const P q = tmp[(start + k) % h];
+    __syncthreads();
+    // Lexicographic minimum: (index of the best) per thread, then the block.
+    long long best = -1;
+    for (long long k = threadIdx.x; k < h; k += blockDim.x)
+        if (best < 0 || lex_less(tmp[k], tmp[best])) best = k;
+    auto better = [&](long long a, long long b) -> long long {  // -1 = none
+        if (a < 0) return b;
+        if (b < 0) return a;
+        return lex_less(tmp[b], tmp[a]) ? b : a;
+    };
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) best = better(best, __shfl_xor_sync(0xffffffffu, best, o));
+    if ((threadIdx.x & 31) == 0) s_best[threadIdx.x >> 5] = best;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        best = threadIdx.x < (blockDim.x >> 5) ? s_best[threadIdx.x] : -1;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) best = better(best, __shfl_xor_sync(0xffffffffu, best, o));
+        if (threadIdx.x == 0) s_best[0] = best;
+    }
+    __syncthreads();
+    const long long start = s_best[0];
+    for (long long k = threadIdx.x; k < h; k += blockDim.x) {
+        long long j = start + k;
+        if (j >= h) j -= h;
+        const P q = tmp[j];
         hull[k] = make_int2((int)q.x, (int)q.y);
     }
-    *h_out = h;
+    if (threadIdx.x == 0) *h_out = h;
+}
+
+constexpr int kLeafThreads = 128;  // leaf threads per CTA: stacks of 128 x 32 x 16 B = 64 KB
+constexpr size_t kLeafSmem = (size_t)kLeafThreads * kLeaf * sizeof(P);
+constexpr int kCoopThreads = 512;
+static_assert((kCoopThreads / 32) * kStage * sizeof(P) <= kLeafSmem, "merge slabs reuse the leaf stacks");
+
+__global__ void __launch_bounds__(kLeafThreads) k_hull_leaf(const int2* __restrict__ lower,
+                                                            const int2* __restrict__ upper,
+                                                            const long long* __restrict__ counts, uint32_t nchunks,
+                                                            uint64_t cap, P* __restrict__ buf,
+                                                            int* __restrict__ cnt) {
+    extern __shared__ P stacks[];
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= nchunks) return;
+    leaf_chunk(lower, upper, counts[1], blockIdx.y, c, nchunks, cap, stacks + threadIdx.x * kLeaf, buf, cnt);
+}
+
+__global__ void __launch_bounds__(256) k_hull_merge(const P* __restrict__ in, const int* __restrict__ cnt_in, P* __restrict__ out,
+                             int* __restrict__ cnt_out, uint32_t nchunks, uint64_t cap, uint32_t nregions,
+                             uint64_t region_cap) {
+    __shared__ P slab[256 / 32][kStage];
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (gw >= 2 * ((nregions + 1) / 2)) return;
+    merge_pair(gw, threadIdx.x & 31, in, cnt_in, out, cnt_out, nchunks, cap, nregions, region_cap,
+               slab[threadIdx.x >> 5]);
+}
+
+__global__ void k_hull_final(const P* __restrict__ fin, const int* __restrict__ cnt_fin, uint32_t nchunks,
+                             uint64_t cap, const long long* __restrict__ counts, int swapped,
+                             P* __restrict__ tmp, int2* __restrict__ hull, long long* __restrict__ h_out) {
+    final_block(fin, cnt_fin, nchunks, cap, counts, swapped, tmp, hull, h_out);
+}
+
+// All of K4 as one cooperative kernel (one CTA per SM): leaves, a grid
+// barrier per merge level (~1.3 us instead of a launch boundary), and the
+// final on CTA 0.
+__global__ void __launch_bounds__(kCoopThreads, 1)
+    k_hull_coop(const int2* __restrict__ lower, const int2* __restrict__ upper, const long long* __restrict__ counts,
+                uint32_t nchunks, uint64_t cap, P* buf0, P* buf1, int* cnt0, int* cnt1, int swapped, P* tmp,
+                int2* __restrict__ hull, long long* __restrict__ h_out, GridBar* bar) {
+    extern __shared__ P stacks[];
+    const long long v = counts[1];
+    if (threadIdx.x < kLeafThreads) {
+        for (uint32_t t = blockIdx.x * kLeafThreads + threadIdx.x; t < 2 * nchunks; t += gridDim.x * kLeafThreads) {
+            const int prob = t >= nchunks;
+            leaf_chunk(lower, upper, v, prob, prob ? t - nchunks : t, nchunks, cap, stacks + threadIdx.x * kLeaf,
+                       buf0, cnt0);
+        }
+    }
+    grid_barrier(bar);
+    P *bin = buf0, *bout = buf1;
+    int *cin = cnt0, *cout = cnt1;
+    uint32_t nregions = nchunks;
+    uint64_t region_cap = kLeaf;
+    const uint32_t warps = gridDim.x * (blockDim.x >> 5);
+    const uint32_t gw0 = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    while (nregions > 1) {
+        const uint32_t npairs = (nregions + 1) / 2;
+        for (uint32_t gw = gw0; gw < 2 * npairs; gw += warps)
+            merge_pair(gw, threadIdx.x & 31, bin, cin, bout, cout, nchunks, cap, nregions, region_cap,
+                       stacks + (threadIdx.x >> 5) * kStage);  // the leaf stacks, free after the leaves
+        grid_barrier(bar);
+        P* tb = bin;
+        bin = bout;
+        bout = tb;
+        int* tc = cin;
+        cin = cout;
+        cout = tc;
+        nregions = npairs;
+        region_cap *= 2;
+    }
+    if (blockIdx.x == 0) final_block(bin, cin, nchunks, cap, counts, swapped, tmp, hull, h_out);
 }
 
 }  // namespace
@@ -213,10 +324,53 @@ extern "C" int chp_hull(chp_ctx* ctx, const int32_t* d_lower, const int32_t* d_u
     P* tmp = (P*)ctx->hull_a.p + 2 * cap;
     const long long* counts = reinterpret_cast<const long long*>(d_counts);
 
-    dim3 lg((nchunks + 127) / 128, 2);
-    k_hull_leaf<<<lg, 128, 0, ctx->stream>>>(reinterpret_cast<const int2*>(d_lower),
-                                             reinterpret_cast<const int2*>(d_upper), counts, nchunks, cap,
-                                             bufs[0], cnts[0]);
+    // CHP_HULL_LAUNCHES=1 (tests): the multi-launch form even when the
+    // cooperative kernel is available.
+    static const bool force_launches = getenv("CHP_HULL_LAUNCHES") != nullptr;
+    if (ctx->coop && !force_launches) {
+        if (!ctx->gridbar.p) {
+            if ((rc = chp_ensure(ctx, ctx->gridbar, 64))) return rc;
+            CHP_CUDA(ctx, cudaMemsetAsync(ctx->gridbar.p, 0, 64, ctx->stream));
+        }
+        if (!ctx->hull_coop_checked) {
+            ctx->hull_coop_checked = 1;
+            int per_sm = 0;
+            if (cudaFuncSetAttribute(k_hull_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLeafSmem) ==
+                    cudaSuccess &&
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hull_coop, kCoopThreads, kLeafSmem) ==
+                    cudaSuccess)
+                ctx->hull_coop_ok = per_sm >= 1;
+            cudaGetLastError();
+        }
+        if (ctx->hull_coop_ok) {
+            const int2* lo = reinterpret_cast<const int2*>(d_lower);
+            const int2* up = reinterpret_cast<const int2*>(d_upper);
+            int2* hp = reinterpret_cast<int2*>(d_hull);
+            long long* hh = reinterpret_cast<long long*>(d_h);
+            GridBar* bar = (GridBar*)ctx->gridbar.p;
+            uint32_t nc = nchunks;
+            uint64_t cp = cap;
+            int sw = swapped;
+            void* args[] = {(void*)&lo,      (void*)&up,      (void*)&counts, (void*)&nc,   (void*)&cp,
+                            (void*)&bufs[0], (void*)&bufs[1], (void*)&cnts[0], (void*)&cnts[1], (void*)&sw,
+                            (void*)&tmp,     (void*)&hp,      (void*)&hh,     (void*)&bar};
+            // (Refused when the grid cannot be co-resident: the launches below.)
+            if (cudaLaunchCooperativeKernel((const void*)k_hull_coop, dim3(ctx->sm_count), dim3(kCoopThreads), args,
+                                            kLeafSmem, ctx->stream) == cudaSuccess) {
+                CHP_LAUNCHED(ctx);
+                return CHP_OK;
+            }
+            cudaGetLastError();
+        }
+    }
+    if (!ctx->hull_leaf_attr) {
+        CHP_CUDA(ctx, cudaFuncSetAttribute(k_hull_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLeafSmem));
+        ctx->hull_leaf_attr = 1;
+    }
+    dim3 lg((nchunks + kLeafThreads - 1) / kLeafThreads, 2);
+    k_hull_leaf<<<lg, kLeafThreads, kLeafSmem, ctx->stream>>>(reinterpret_cast<const int2*>(d_lower),
+                                                              reinterpret_cast<const int2*>(d_upper), counts,
+                                                              nchunks, cap, bufs[0], cnts[0]);
     CHP_LAUNCHED(ctx);
     int cur = 0;
     uint32_t nregions = nchunks;
@@ -232,8 +386,8 @@ extern "C" int chp_hull(chp_ctx* ctx, const int32_t* d_lower, const int32_t* d_u
         nregions = npairs;
         region_cap *= 2;
     }
-    k_hull_final<<<1, 32, 0, ctx->stream>>>(bufs[cur], cnts[cur], nchunks, cap, counts, swapped, tmp,
-                                            reinterpret_cast<int2*>(d_hull), reinterpret_cast<long long*>(d_h));
+    k_hull_final<<<1, 1024, 0, ctx->stream>>>(bufs[cur], cnts[cur], nchunks, cap, counts, swapped, tmp,
+                                              reinterpret_cast<int2*>(d_hull), reinterpret_cast<long long*>(d_h));
     CHP_LAUNCHED(ctx);
     return CHP_OK;
 }

@@ -1045,33 +1045,9 @@ __global__ void __launch_bounds__(kThreads) k_reduce_sampled(const int32_t* __re
 // the columns -> grid barrier -> every CTA loads the merged table -> main
 // pass.  Saves two launch boundaries (ramp-down/ramp-up) and spreads the
 // merge over every SM.
-struct GridBar {
-    unsigned long long count;  // arrivals since the context was created (see grid_barrier)
-};
-
+// (GridBar / grid_barrier: chp_internal.cuh, shared with the cooperative K4.)
 constexpr size_t kFusedMergeSmem = 16 * 64 * sizeof(uint4);  // phase B partials
 
-__device__ __forceinline__ void grid_barrier(GridBar* b) {
-    // One atomic per CTA and no reset: arrival k of barrier round r sees
-    // old = r * G + k, and the round is complete once the 64-bit counter
-    // reaches (r + 1) * G.  Every cooperative launch on a context uses the
-    // same grid size G (one CTA per SM).  The last arrival's add releases
-    // everyone directly (the reset-and-flip form needed two more serialised
-    // L2 round trips, ~2 us at 148 CTAs).
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        const unsigned long long G = gridDim.x;
-        const unsigned long long old = atomicAdd(&b->count, 1ull);
-        const unsigned long long target = old - old % G + G;
-        unsigned long long cur;
-        do {
-            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(cur) : "l"(&b->count) : "memory");
-        } while (cur < target);
-        __threadfence();
-    }
-    __syncthreads();
-}
 
 // Out of line so phases A-C do not constrain the main pass's registers.
 __device__ __noinline__ void sampled_main_pass(const int32_t* __restrict__ xy, uint64_t n, Geo g, uint32_t width,

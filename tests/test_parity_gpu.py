@@ -250,3 +250,35 @@ def test_full_size_properties(ctx, config):
     assert 0 < s <= 2 * p
     again = ctx.reduce(comp["chain"][:s].contiguous(), p, q=p)
     assert torch.equal(again, ref_dl)
+
+
+def test_hull_multi_launch_form():
+    """K4 runs as one cooperative kernel when it can; the per-stage launch
+    form (CHP_HULL_LAUNCHES=1, read once per process) must agree."""
+    import os
+    import subprocess
+    import sys
+
+    code = r"""
+import numpy as np, torch, sys
+sys.path.insert(0, %r)
+import oracle
+from paper_1505_00914_b200.device import Context, generate_host
+orc = oracle.Oracle()
+ctx = Context(0)
+for config, p, n in ((2, 65536, 2_000_000), (3, 16384, 2_000_000), (4, 1 << 20, 2_000_000), (5, 256, 100_000)):
+    xy = generate_host(config, config, p, n)
+    DL = ctx.reduce(torch.from_numpy(xy).cuda(), p, q=p)
+    comp = ctx.compact(DL, p, chain=True, lower=True, upper=True)
+    hull = ctx.hull(comp, p)
+    torch.cuda.synchronize()
+    h = int(hull["h"].item())
+    s = int(comp["counts"][0].item())
+    chain = comp["chain"][:s].cpu().numpy()
+    assert np.array_equal(hull["hull"][:h].cpu().numpy(), orc.melkman(chain)), config
+print("ok")
+""" % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for env in ({"CHP_HULL_LAUNCHES": "1"}, {}):
+        r = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env}, capture_output=True, text=True,
+                           timeout=600)
+        assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
