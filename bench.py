@@ -377,9 +377,10 @@ def main():
         e2e = {"value": total_points / (e2e_ms * 1e-3) / 1e9, "unit": "Gpoints/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": int(s_out[0]) * 8 + 64, "ms_per_step": e2e_ms,
                "path": "chp_pipeline_host (pinned int32 input; "
-                       + ("8 Mi-point chunks packed to 16-bit slot|y words on host threads (AVX2), int32 chunks "
-                          "DMA'd from the input's end while the host packs, " if h2d < n * 8 else
-                          "16 Mi-point int32 chunks, ")
+                       + (("8 Mi-point chunks packed to 16-bit slot|y words" if p <= 65536 else
+                           "8 Mi-point chunks packed to 42-bit slot|y points, 3 per 16 bytes")
+                          + " on host threads, int32 chunks DMA'd from the input's end while the host packs, "
+                          if h2d < n * 8 else "16 Mi-point int32 chunks, ")
                        + "H2D overlapped with K1)"}
         # The reference's main entry, reducer::precondition (bounds unknown:
         # one pass computes them, then fold and compaction), through the same
@@ -400,8 +401,9 @@ def main():
             precondition_e2e = {"value": n / (pre_ms * 1e-3) / 1e9, "unit": "Gpoints/s", "ms_per_step": pre_ms,
                                 "h2d_bytes_per_step": ctx.last_h2d_bytes,
                                 "path": "chp_precondition_run + chp_last_outputs (pinned int32 input, bounds "
-                                        "unknown: one pass, speculative 16-bit packing against a window from a "
-                                        "64 Ki-point prefix, the bounds folded as the chunks land)"}
+                                        "unknown: one pass, speculative 16-bit (or 42-bit) packing against a "
+                                        "2^16 (2^21) window from a 64 Ki-point prefix, the bounds folded as the "
+                                        "chunks land)"}
         del host
 
     base = None

@@ -310,6 +310,42 @@ uint32_t pack_any(const HostPts& in, uint64_t off, uint64_t m, uint32_t* __restr
     return bad;
 }
 
+// 42-bit packing (width and y range up to 2^21 each, e.g. C4's 2^20 x 2^20):
+// v = slot | (y - ybase) << 21, three points per 16-byte word (lo64 = v0 |
+// v1 << 42, hi64 = v1 >> 22 | v2 << 20; k_unpack42 in misc.cu), 5.33 bytes
+// per point instead of 8.  m need not be a multiple of 3 (the last word is
+// zero-padded); dst holds (m + 2) / 3 words.
+uint32_t pack42_any(const HostPts& in, uint64_t off, uint64_t m, uint64_t* __restrict__ dst, uint32_t base,
+                    uint32_t ybase, uint32_t wcheck, uint32_t qmax) {
+    uint32_t bad = 0;
+    auto val = [&](uint64_t k) -> uint64_t {
+        uint64_t s, t;
+        if (in.p32) {
+            s = (uint32_t)in.p32[2 * (off + k)] - base;
+            t = (uint32_t)in.p32[2 * (off + k) + 1] - ybase;
+        } else {
+            s = (uint64_t)(in.x(off + k) - (int64_t)(int32_t)base);
+            t = (uint64_t)(in.y(off + k) - (int64_t)(int32_t)ybase);
+        }
+        bad |= (uint32_t)(s >= wcheck) | (uint32_t)(t >= qmax);
+        return (s & 0x1FFFFF) | ((t & 0x1FFFFF) << 21);
+    };
+    const uint64_t full = m / 3;
+    for (uint64_t w = 0; w < full; ++w) {
+        const uint64_t v0 = val(3 * w), v1 = val(3 * w + 1), v2 = val(3 * w + 2);
+        const __m128i q = _mm_set_epi64x((long long)((v1 >> 22) | (v2 << 20)), (long long)(v0 | (v1 << 42)));
+        _mm_stream_si128(reinterpret_cast<__m128i*>(dst + 2 * w), q);
+    }
+    if (m % 3) {
+        uint64_t v[3] = {0, 0, 0};
+        for (uint64_t k = 3 * full; k < m; ++k) v[k - 3 * full] = val(k);
+        dst[2 * full] = v[0] | (v[1] << 42);
+        dst[2 * full + 1] = (v[1] >> 22) | (v[2] << 20);
+    }
+    _mm_sfence();
+    return bad;
+}
+
 // Packed form of stream_chunks for width <= 2^16 and 1 <= y <= q <= 2^16:
 // host workers pack chunk k into pinned 4-byte/point staging while the DMA
 // of chunk k-1 is in flight, so PCIe carries half the bytes; on the device
@@ -322,22 +358,30 @@ uint32_t pack_any(const HostPts& in, uint64_t off, uint64_t m, uint32_t* __restr
 // engine would idle during each pack; it is kept busy with int32 chunks
 // DMA'd straight from the END of the input (K1 validates those itself), so
 // the packed front and the raw back meet where both resources finish.
+//
+// wide = true: the 42-bit form (three points per 16-byte word) for ranges up
+// to 2^21 x 2^21 (not speculative).
 template <typename Launch>
 int stream_chunks_packed(chp_ctx* ctx, const HostPts& in, uint64_t n, int64_t x_off, int32_t ybase,
                          uint32_t wcheck, uint32_t qmax, bool speculative, bool* bad, Launch&& launch,
-                         int32_t* d_dest = nullptr) {
+                         int32_t* d_dest = nullptr, bool wide = false) {
     *bad = false;
     if (n == 0) return CHP_OK;
+    // packed bytes of m points; part boundaries within a chunk keep whole words
+    auto pbytes = [&](uint64_t m) -> uint64_t { return wide ? (m + 2) / 3 * 16 : m * 4; };
+    const uint64_t align = wide ? 24 : 8;
+    double& rate = wide ? ctx->pack_rate42 : ctx->pack_rate;
     // 8 Mi points per chunk (e2e C2, hybrid: 2 Mi 8.7-9.1, 4 Mi 9.4-9.7, 8 Mi
     // 9.9, 16 Mi 10.0 Gpts/s; smaller chunks pay the per-chunk dispatch).
     constexpr uint64_t kPackChunk = 8ull << 20;
     constexpr double kPcieBps = 50e9;  // H2D bytes / s (PCIe 5 x16, measured ~55e9)
-    const uint64_t chunk = std::min<uint64_t>(kPackChunk, n);
+    // (42-bit: whole 3-point words per chunk, so only the input's last word pads)
+    const uint64_t chunk = std::min<uint64_t>(wide ? kPackChunk / 24 * 24 : kPackChunk, n);
     const bool pinned = in.pinned32();
     const bool hybrid = pinned;
     int rc;
     for (int b = 0; b < 2; ++b) {
-        if ((rc = chp_ensure(ctx, ctx->stage_dev[b], (size_t)chunk * 4))) return rc;
+        if ((rc = chp_ensure(ctx, ctx->stage_dev[b], (size_t)pbytes(chunk)))) return rc;
         if ((rc = chp_ensure(ctx, ctx->unpack_dev[b], (size_t)chunk * 8))) return rc;
         if ((hybrid || speculative) && (rc = chp_ensure(ctx, ctx->raw_dev[b], (size_t)chunk * 8))) return rc;
         if ((hybrid || speculative) && !ctx->ev_rcopied[b]) {
@@ -345,13 +389,13 @@ int stream_chunks_packed(chp_ctx* ctx, const HostPts& in, uint64_t n, int64_t x_
             CHP_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_rconsumed[b], cudaEventDisableTiming));
         }
     }
-    if (ctx->pack_bytes < (size_t)chunk * 4) {
+    if (ctx->pack_bytes < (size_t)pbytes(chunk)) {
         for (int b = 0; b < 2; ++b) {
             if (ctx->pack_host[b]) cudaFreeHost(ctx->pack_host[b]);
             ctx->pack_host[b] = nullptr;
         }
-        for (int b = 0; b < 2; ++b) CHP_CUDA(ctx, cudaMallocHost(&ctx->pack_host[b], (size_t)chunk * 4));
-        ctx->pack_bytes = (size_t)chunk * 4;
+        for (int b = 0; b < 2; ++b) CHP_CUDA(ctx, cudaMallocHost(&ctx->pack_host[b], (size_t)pbytes(chunk)));
+        ctx->pack_bytes = (size_t)pbytes(chunk);
     }
     HostPool* pool = pool_of(ctx);
     const uint32_t base = (uint32_t)(int32_t)(x_off + 1);
@@ -423,7 +467,7 @@ int stream_chunks_packed(chp_ctx* ctx, const HostPts& in, uint64_t n, int64_t x_
         const uint64_t m = std::min<uint64_t>(chunk, back - front);
         if (hybrid) {
             // Keep the copy engine busy for the duration of this pack.
-            const double t_pack = (double)m / ctx->pack_rate;
+            const double t_pack = (double)m / rate;
             if (t_pack > dma_ahead && (rc = raw_fill(t_pack - dma_ahead))) return rc;
             if (front >= back) break;
         }
@@ -432,18 +476,21 @@ int stream_chunks_packed(chp_ctx* ctx, const HostPts& in, uint64_t n, int64_t x_
         // The DMA out of this staging buffer (two packed chunks ago) must be done.
         CHP_CUDA(ctx, cudaEventSynchronize(ctx->ev_copied[b]));
         uint32_t* dst = static_cast<uint32_t*>(ctx->pack_host[b]);
+        uint64_t* dst64 = static_cast<uint64_t*>(ctx->pack_host[b]);
         const int parts = pool->parts_for(mm);
         const auto t0 = std::chrono::steady_clock::now();
         std::fill(part_bad.begin(), part_bad.end(), 0u);
         pool->run(
             [&](int i) {
-                const uint64_t lo = (mm * (uint64_t)i / parts) & ~7ull;
-                const uint64_t hi = i + 1 == parts ? mm : (mm * (uint64_t)(i + 1) / parts) & ~7ull;
-                part_bad[(size_t)i] = pack_any(in, front + lo, hi - lo, dst + lo, base, (uint32_t)ybase, wcheck, qmax);
+                const uint64_t lo = mm * (uint64_t)i / parts / align * align;
+                const uint64_t hi = i + 1 == parts ? mm : mm * (uint64_t)(i + 1) / parts / align * align;
+                part_bad[(size_t)i] =
+                    wide ? pack42_any(in, front + lo, hi - lo, dst64 + 2 * (lo / 3), base, (uint32_t)ybase, wcheck, qmax)
+                         : pack_any(in, front + lo, hi - lo, dst + lo, base, (uint32_t)ybase, wcheck, qmax);
             },
             parts);
         const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-        if (mm >= (1u << 20) && dt > 0) ctx->pack_rate = 0.5 * ctx->pack_rate + 0.5 * (double)mm / dt;
+        if (mm >= (1u << 20) && dt > 0) rate = 0.5 * rate + 0.5 * (double)mm / dt;
         uint32_t chunk_bad = 0;
         for (uint32_t v : part_bad) chunk_bad |= v;
         if (chunk_bad && speculative) {  // not 16-bit: the chunk goes as int32 pairs
@@ -454,14 +501,15 @@ int stream_chunks_packed(chp_ctx* ctx, const HostPts& in, uint64_t n, int64_t x_
         }
         any_bad |= chunk_bad;
         CHP_CUDA(ctx, cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_consumed[b], 0));
-        CHP_CUDA(ctx, cudaMemcpyAsync(ctx->stage_dev[b].p, dst, (size_t)mm * 4, cudaMemcpyHostToDevice,
+        CHP_CUDA(ctx, cudaMemcpyAsync(ctx->stage_dev[b].p, dst, (size_t)pbytes(mm), cudaMemcpyHostToDevice,
                                       ctx->copy_stream));
-        ctx->h2d_bytes += (uint64_t)mm * 4;
-        dma_ahead = (double)mm * 4 / kPcieBps;
+        ctx->h2d_bytes += pbytes(mm);
+        dma_ahead = (double)pbytes(mm) / kPcieBps;
         CHP_CUDA(ctx, cudaEventRecord(ctx->ev_copied[b], ctx->copy_stream));
         CHP_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_copied[b], 0));
-        if ((rc = chp_unpack16(ctx, (const uint32_t*)ctx->stage_dev[b].p, mm, (int32_t)base, ybase,
-                               d_dest ? d_dest + 2 * front : (int32_t*)ctx->unpack_dev[b].p)))
+        int32_t* udst = d_dest ? d_dest + 2 * front : (int32_t*)ctx->unpack_dev[b].p;
+        if ((rc = wide ? chp_unpack42(ctx, ctx->stage_dev[b].p, mm, (int32_t)base, ybase, udst)
+                       : chp_unpack16(ctx, (const uint32_t*)ctx->stage_dev[b].p, mm, (int32_t)base, ybase, udst)))
             return rc;
         CHP_CUDA(ctx, cudaEventRecord(ctx->ev_consumed[b], ctx->stream));
         if ((rc = launch(d_dest ? (const int32_t*)(d_dest + 2 * front) : (const int32_t*)ctx->unpack_dev[b].p, mm)))
@@ -475,7 +523,7 @@ int stream_chunks_packed(chp_ctx* ctx, const HostPts& in, uint64_t n, int64_t x_
 // A 2^16 x 2^16 packing window from the box of the first min(n, 64 Ki)
 // points, centred in the slack; false when that prefix is already wider or
 // taller than 2^16.
-bool pack_window(chp_ctx* ctx, const HostPts& in, uint64_t n, int64_t* wx, int64_t* wy) {
+bool pack_window(chp_ctx* ctx, const HostPts& in, uint64_t n, int64_t* wx, int64_t* wy, int64_t W = 65536) {
     (void)ctx;
     const uint64_t m = std::min<uint64_t>(n, 1ull << 16);  // a 64 Ki-point prefix, on the caller's thread
     int64_t b[4] = {INT64_MAX, INT64_MIN, INT64_MAX, INT64_MIN};
@@ -486,12 +534,12 @@ bool pack_window(chp_ctx* ctx, const HostPts& in, uint64_t n, int64_t* wx, int64
         b[2] = std::min(b[2], y);
         b[3] = std::max(b[3], y);
     }
-    auto place = [](int64_t lo, int64_t hi, int64_t* base) {
+    auto place = [W](int64_t lo, int64_t hi, int64_t* base) {
         const int64_t ext = hi - lo + 1;
-        if (ext > 65536 || lo < INT32_MIN || hi > INT32_MAX) return false;
-        int64_t s = lo - (65536 - ext) / 2;
+        if (ext > W || lo < INT32_MIN || hi > INT32_MAX) return false;
+        int64_t s = lo - (W - ext) / 2;
         s = std::max<int64_t>(s, INT32_MIN);
-        s = std::min<int64_t>(s, (int64_t)INT32_MAX - 65535);
+        s = std::min<int64_t>(s, (int64_t)INT32_MAX - (W - 1));
         *base = s;
         return true;
     };
@@ -517,9 +565,14 @@ int stream_reduce(chp_ctx* ctx, const HostPts& in, uint64_t n, int64_t width, in
                           !(flags & CHP_PIPELINE_NO_PACK) && !std::getenv("CHP_PIPELINE_NO_PACK") &&
                           x_off + 1 >= (int64_t)INT32_MIN && x_off <= (int64_t)INT32_MAX &&
                           ybase >= (int64_t)INT32_MIN && ybase <= (int64_t)INT32_MAX;
+    // Known ranges up to 2^21 x 2^21 (e.g. C4: 2^20 x 2^20): the 42-bit form.
+    const bool packable42 = !packable && !speculative && width <= (1 << 21) && ycount >= 1 && ycount <= (1 << 21) &&
+                            !(flags & CHP_REDUCE_NO_VALIDATE) && !(flags & CHP_PIPELINE_NO_PACK) &&
+                            !std::getenv("CHP_PIPELINE_NO_PACK") && x_off + 1 >= (int64_t)INT32_MIN &&
+                            x_off <= (int64_t)INT32_MAX && ybase >= (int64_t)INT32_MIN && ybase <= (int64_t)INT32_MAX;
     bool bad = false;
     int rc;
-    if (!packable) {
+    if (!packable && !packable42) {
         uint32_t nb = 0;  // int64 input: a coordinate beyond int32
         if ((rc = stream_chunks(ctx, in, n, launch, nullptr, &nb))) return rc;
         bad = nb != 0;
@@ -527,7 +580,8 @@ int stream_reduce(chp_ctx* ctx, const HostPts& in, uint64_t n, int64_t width, in
         const uint32_t wcheck = (uint32_t)std::min<int64_t>(width, (int64_t)INT32_MAX - x_off);
         const uint32_t qmax =
             (uint32_t)std::min<int64_t>(speculative ? 65536 : ycount, (int64_t)INT32_MAX - ybase + 1);
-        if ((rc = stream_chunks_packed(ctx, in, n, x_off, (int32_t)ybase, wcheck, qmax, speculative, &bad, launch)))
+        if ((rc = stream_chunks_packed(ctx, in, n, x_off, (int32_t)ybase, wcheck, qmax, speculative, &bad, launch,
+                                       nullptr, packable42)))
             return rc;
     }
     if (bad) {  // same outcome as the unpacked path: the error word of DL
@@ -812,12 +866,16 @@ static int precondition_core(chp_ctx* ctx, const HostPts& in, uint64_t n, int64_
         // box (centred in the 2^16 slack) packs every chunk that fits, the
         // rest travel as int32 pairs; either way they land unpacked in the
         // resident buffer.
+        // A prefix wider than 2^16 tries a 2^21 window and the 42-bit form.
         int64_t wx = 0, wy = 0;
-        const bool win = !std::getenv("CHP_PIPELINE_NO_PACK") && pack_window(ctx, in, n, &wx, &wy);
+        const bool pack = !std::getenv("CHP_PIPELINE_NO_PACK");
+        const bool win = pack && pack_window(ctx, in, n, &wx, &wy);
+        const bool win42 = pack && !win && pack_window(ctx, in, n, &wx, &wy, 1 << 21);
         bool narrow_bad = false;  // int64 input: a coordinate beyond int32
-        if (win) {
-            if ((rc = stream_chunks_packed(ctx, in, n, wx - 1, (int32_t)wy, 65536u, 65536u, true, &narrow_bad, fold,
-                                           (int32_t*)pts.p)))
+        if (win || win42) {
+            const uint32_t W = win ? 65536u : (1u << 21);
+            if ((rc = stream_chunks_packed(ctx, in, n, wx - 1, (int32_t)wy, W, W, true, &narrow_bad, fold,
+                                           (int32_t*)pts.p, win42)))
                 return rc;
         } else {
             uint32_t nb = 0;

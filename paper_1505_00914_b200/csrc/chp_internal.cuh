@@ -65,7 +65,8 @@ struct chp_ctx {
     int64_t last_width = 0, last_s = 0, last_h = -1;
     cudaEvent_t ev_rcopied[2] = {nullptr, nullptr};
     cudaEvent_t ev_rconsumed[2] = {nullptr, nullptr};
-    double pack_rate = 8e9;  // points / s
+    double pack_rate = 8e9;    // points / s, 16-bit packing
+    double pack_rate42 = 6e9;  // points / s, 42-bit packing
     // Launch-setup cache (reduce.cu kernel_blocks): kernel -> (dynamic smem
     // it was configured for, resident blocks per SM at that size).
     std::unordered_map<const void*, std::pair<size_t, int>> kcache;
@@ -114,6 +115,8 @@ int chp_bounds_accumulate(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int32_t
 // Packed host pipeline (abi.cu): 32-bit words (slot | (y - 1) << 16) back to
 // int32 (x, y) pairs with x = slot + base.
 int chp_unpack16(chp_ctx* ctx, const uint32_t* d_in, uint64_t n, int32_t base, int32_t ybase, int32_t* d_out);
+// The same for 42-bit points (slot | (y - ybase) << 21), three per 16-byte word.
+int chp_unpack42(chp_ctx* ctx, const void* d_in, uint64_t n, int32_t base, int32_t ybase, int32_t* d_out);
 // K1 with a general valid y range [ybase, ybase + ycount) (reduce.cu).
 int chp_reduce_yr(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t width, int64_t ybase, int64_t ycount,
                   int64_t x_off, int32_t* d_L, uint32_t flags);

@@ -146,7 +146,35 @@ __global__ void k_unpack16(const uint4* __restrict__ in4, uint64_t n4, const uin
         for (uint64_t i = 4 * n4 + threadIdx.x; i < n; i += blockDim.x)
             out[i] = make_int2((int)(in[i] & 0xFFFFu) + base, (int)(in[i] >> 16) + ybase);
 }
+// 42-bit form for ranges up to 2^21 x 2^21: point v = slot | (y - ybase) << 21,
+// three per 16-byte word: lo64 = v0 | v1 << 42, hi64 = v1 >> 22 | v2 << 20.
+__global__ void k_unpack42(const uint4* __restrict__ in, uint64_t n, int32_t base, int32_t ybase,
+                           int2* __restrict__ out) {
+    const uint64_t nw = (n + 2) / 3;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    constexpr uint64_t M21 = (1ull << 21) - 1, M42 = (1ull << 42) - 1;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nw; i += stride) {
+        const uint4 q = __ldcs(in + i);
+        const uint64_t lo = (uint64_t)q.x | ((uint64_t)q.y << 32), hi = (uint64_t)q.z | ((uint64_t)q.w << 32);
+        const uint64_t v[3] = {lo & M42, (lo >> 42) | ((hi << 22) & M42), hi >> 20};
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const uint64_t j = 3 * i + k;
+            if (j < n) out[j] = make_int2((int)(uint32_t)(v[k] & M21) + base, (int)(uint32_t)(v[k] >> 21) + ybase);
+        }
+    }
+}
 }  // namespace
+
+int chp_unpack42(chp_ctx* ctx, const void* d_in, uint64_t n, int32_t base, int32_t ybase, int32_t* d_out) {
+    if (n == 0) return CHP_OK;
+    const uint64_t nw = (n + 2) / 3;
+    const int blocks = (int)std::min<uint64_t>((nw + 255) / 256, (uint64_t)ctx->sm_count * 8);
+    k_unpack42<<<blocks, 256, 0, ctx->stream>>>(reinterpret_cast<const uint4*>(d_in), n, base, ybase,
+                                                reinterpret_cast<int2*>(d_out));
+    CHP_LAUNCHED(ctx);
+    return CHP_OK;
+}
 
 int chp_unpack16(chp_ctx* ctx, const uint32_t* d_in, uint64_t n, int32_t base, int32_t ybase, int32_t* d_out) {
     if (n == 0) return CHP_OK;

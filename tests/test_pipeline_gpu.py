@@ -77,12 +77,51 @@ def test_pipeline_host_packed_sizes(ctx, orc, n, pinned):
 def test_pipeline_host_unpacked_when_wide(ctx, orc):
     p = 65536
     xy = generate_host(2, 2, p, 100_000)
-    xy[:, 1] = xy[:, 1] * 2  # y up to 2^17: q > 2^16 -> int32 transfer
-    out = ctx.pipeline_host(xy, p, 2 * p, L=True, chain=True)
+    xy[:, 1] = xy[:, 1] * 64  # y up to 2^22: q > 2^21 -> int32 transfer
+    out = ctx.pipeline_host(xy, p, 64 * p, L=True, chain=True)
     assert ctx.last_h2d_bytes == 8 * len(xy)
-    ref = orc.pipeline(xy, p, 2 * p)
+    ref = orc.pipeline(xy, p, 64 * p)
     assert np.array_equal(out["L"], ref["L"])
     assert np.array_equal(out["chain"], ref["chain"])
+
+
+# Known ranges up to 2^21 x 2^21 travel as 42-bit points, three per 16 bytes.
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 1001, 8_388_608 + 5, 20_000_001])
+@pytest.mark.parametrize("pinned", [False, True])
+def test_pipeline_host_packed42(ctx, orc, n, pinned):
+    p = 1 << 20
+    xy = generate_host(4, 4, p, n)
+    if pinned:
+        xy = _pinned(xy)
+    out = ctx.pipeline_host(xy, p, p, L=True, chain=True, hull=True)
+    if not pinned:  # (pinned input: part of it goes as int32 pairs from the end)
+        assert ctx.last_h2d_bytes == (n + 2) // 3 * 16
+    ref = orc.pipeline(xy, p, p)
+    assert np.array_equal(out["L"], ref["L"])
+    assert np.array_equal(out["chain"], ref["chain"])
+    assert np.array_equal(out["hull"], ref["hull"])
+
+
+def test_pipeline_host_packed42_extremes(ctx, orc):
+    # the 21-bit fields at both ends, in every position of a 3-point word
+    p, q = 1 << 21, 1 << 21
+    base = np.array([[1, 1], [1, q], [p, 1], [p, q], [300, 7], [p - 1, q - 1], [2, 2]], np.int32)
+    for shift in range(3):
+        xy = np.concatenate([np.full((shift, 2), 5, np.int32), np.repeat(base, 301, axis=0)])
+        out = ctx.pipeline_host(xy, p, q, L=True, chain=True)
+        ref = orc.pipeline(xy, p, q)
+        assert np.array_equal(out["L"], ref["L"])
+        assert np.array_equal(out["chain"], ref["chain"])
+
+
+@pytest.mark.parametrize("bad", [(0, 5), ((1 << 20) + 1, 5), (7, 0), (7, (1 << 20) + 1), (-2**31, 1)])
+@pytest.mark.parametrize("where", [0, 1, 2, 999_999])
+def test_pipeline_host_packed42_invalid_raises(ctx, bad, where):
+    p = 1 << 20
+    xy = generate_host(4, 4, p, 1_000_000)
+    xy[where] = bad
+    with pytest.raises(ValueError):
+        ctx.pipeline_host(xy, p, p)
 
 
 @pytest.mark.parametrize("bad", [(0, 5), (4097, 5), (7, 0), (7, 4097), (-2**31, 1), (2**31 - 1, 2**31 - 1)])
@@ -216,6 +255,28 @@ def test_precondition_speculative_window(ctx, orc, pinned):
         xy = _pinned(xy)
     out = ctx.precondition_host(xy, chain=True, hull=True)
     assert 4 * n < ctx.last_h2d_bytes <= 8 * n  # some chunks packed, some not
+    ref = orc.precondition(xy)
+    assert out["bbox"] == ref["bbox"]
+    assert np.array_equal(out["chain"], ref["chain"])
+    assert np.array_equal(out["hull"], ref["hull"])
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_precondition_speculative_window42(ctx, orc, pinned):
+    # A prefix wider than 2^16 takes a 2^21 window and the 42-bit form; a later
+    # chunk that leaves the window (a 2^24-wide spread after 12 M points) goes
+    # as int32 pairs, and its points still count.
+    rng = np.random.default_rng(78)
+    n = 20_000_000
+    xy = np.empty((n, 2), np.int32)
+    xy[:12_000_000, 0] = rng.integers(-400_000, 300_000, 12_000_000)
+    xy[:12_000_000, 1] = rng.integers(5, 900_000, 12_000_000)
+    xy[12_000_000:, 0] = rng.integers(-(1 << 23), 1 << 23, n - 12_000_000)
+    xy[12_000_000:, 1] = rng.integers(-(1 << 23), 1 << 23, n - 12_000_000)
+    if pinned:
+        xy = _pinned(xy)
+    out = ctx.precondition_host(xy, chain=True, hull=True)
+    assert 16 * n // 3 < ctx.last_h2d_bytes < 8 * n  # some chunks packed (42-bit), some not
     ref = orc.precondition(xy)
     assert out["bbox"] == ref["bbox"]
     assert np.array_equal(out["chain"], ref["chain"])
