@@ -487,9 +487,14 @@ __device__ __forceinline__ uint32_t lds_w(uint32_t addr) {
 template <typename W>
 __global__ void __launch_bounds__(256) k_filter_build(const int* __restrict__ DL, uint32_t width, uint32_t gshift,
                                                       int32_t ybase, uint32_t ys, W* __restrict__ F,
-                                                      uint32_t ngroups) {
+                                                      uint32_t ngroups, const int2* __restrict__ qs) {
     const uint32_t gi = blockIdx.x * blockDim.x + threadIdx.x;
     if (gi > ngroups) return;
+    if (qs) {  // q unset: the speculative bucket range (k_quant_shift)
+        const int2 v = __ldcg(qs);
+        ybase = v.x;
+        ys = (uint32_t)v.y;
+    }
     const uint32_t c0 = gi << gshift;
     const uint32_t c1 = c0 + (1u << gshift);
     W word = FW<W>::kNever;
@@ -548,11 +553,11 @@ __global__ void __launch_bounds__(256) k_filter_build(const int* __restrict__ DL
 // plus the load pipeline need more than 64 registers per thread (at 1024
 // threads it spilled 32 B; C4: 768 656, 896 663, 1024 657 Gpts/s).
 constexpr int kThreadsRF = 896;
-template <typename W, bool READ_FIRST, bool TMA>
+template <typename W, bool READ_FIRST, bool TMA, bool SPEC>
 __global__ void __launch_bounds__((READ_FIRST && !TMA) ? kThreadsRF : kThreads) k_reduce_filter(const int32_t* __restrict__ xy, uint64_t n,
                                                             Geo g, uint32_t width, uint32_t gshift, uint32_t ys,
                                                             const W* __restrict__ F, uint32_t ngroups, int stages,
-                                                            int* __restrict__ DL) {
+                                                            int* __restrict__ DL, const int2* __restrict__ qs) {
     extern __shared__ uint4 sF4[];
     W* sF = reinterpret_cast<W*>(sF4);
     const uint32_t nwords = ngroups + 1;
@@ -568,6 +573,15 @@ __global__ void __launch_bounds__((READ_FIRST && !TMA) ? kThreadsRF : kThreads) 
             for (uint32_t i = threadIdx.x; i < nwords; i += blockDim.x) sF[i] = FW<W>::kNever;
         }
     }
+    // Bucket base: the valid range's (q known), or the speculative range's
+    // (q unset: k_quant_shift); a y below it wraps past every bucket and
+    // misses, one above it has u > every fb and misses.
+    uint32_t qb = g.ybase;
+    if (SPEC) {
+        const int2 v = __ldcg(qs);
+        qb = (uint32_t)v.x;
+        ys = (uint32_t)v.y;
+    }
     __syncthreads();
     constexpr uint32_t H = FW<W>::kHalf, HM = FW<W>::kMask;
     const uint32_t tbase = (uint32_t)__cvta_generic_to_shared(sF4);
@@ -578,7 +592,7 @@ __global__ void __launch_bounds__((READ_FIRST && !TMA) ? kThreadsRF : kThreads) 
     auto test = [&](int32_t x, int32_t y, uint32_t& s, uint32_t& w) -> bool {
         s = min(slot_of(x, g.base), width);
         w = lds_w<W>(tbase + (s >> gshift) * (uint32_t)sizeof(W));
-        return (((uint32_t)y - g.ybase) >> ys) - (w & HM) >= (w >> H);
+        return (((uint32_t)y - qb) >> ys) - (w & HM) >= (w >> H);
     };
     auto valid = [&](uint32_t s, int32_t y) {
         const bool ok = (s < g.wcheck) & ((uint32_t)y - g.ybase < g.qmax);
@@ -590,8 +604,13 @@ __global__ void __launch_bounds__((READ_FIRST && !TMA) ? kThreadsRF : kThreads) 
     // y >= max_lo, so only hi can move.
     auto settle_red = [&](uint32_t s, int32_t y, uint32_t w) {
         if (!valid(s, y)) return;
-        const uint32_t u = ((uint32_t)y - g.ybase) >> ys;
         const uint32_t fa = w & HM, span = w >> H;
+        if (SPEC && y < (int32_t)qb) {  // below the speculative range: below max_lo's bucket, <= min_hi
+            red_min(DL + 2ull * s, y);
+            if (span == 0) red_min(DL + 2ull * s + 1, ~y);
+            return;
+        }
+        const uint32_t u = ((uint32_t)y - qb) >> ys;
         if (span == 0 || u > fa) red_min(DL + 2ull * s + 1, ~y);  // not known below min_hi
         if (span == 0 || u < fa) red_min(DL + 2ull * s, y);       // not known above max_lo
     };
@@ -734,6 +753,35 @@ __device__ __forceinline__ Quant resolve_quant(Quant qz, const int2* __restrict_
     }
     __syncthreads();
     return s_q;
+}
+
+// The group filter's form of the same (one CTA): {base, ys} with the
+// speculative range >> ys <= kmask, written to qs for every later kernel.
+__global__ void k_quant_shift(const int2* __restrict__ part, uint32_t np, Geo g, uint32_t kmask,
+                              int2* __restrict__ qs) {
+    int lo = INT_MAX, hi = INT_MIN;
+    for (uint32_t i = threadIdx.x; i < np; i += 32) {
+        const int2 v = part[i];
+        lo = min(lo, v.x);
+        hi = max(hi, v.y);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if (threadIdx.x == 0) {
+        uint64_t ext;
+        if (lo > hi) {
+            lo = (int)g.ybase;
+            ext = (uint64_t)g.qmax - 1;
+        } else {
+            ext = (uint64_t)((int64_t)hi - lo);
+        }
+        uint32_t ys = 0;
+        while ((ext >> ys) > kmask) ++ys;
+        *qs = make_int2(lo, (int)ys);
+    }
 }
 
 // Phase helpers shared by the three-launch pipeline and the fused kernel.
@@ -1271,11 +1319,25 @@ int kernel_blocks(chp_ctx* ctx, const void* fn, size_t smem, int cap_per_sm, int
 // against a fresh snapshot of DL.  The table (W = 16-bit
 // words with 8-bit halves, or 32-bit words with 16-bit halves) is sized to
 // `fbudget` bytes; the rest of shared memory holds the TMA ring.
-template <typename W>
+template <typename W, bool SPEC>
 int run_group_filter(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, const Geo& g, uint32_t w, int64_t q,
                      uint32_t flags, size_t fbudget, int32_t* d_L) {
     uint32_t ys = 0;
-    while ((uint64_t)(q - 1) >> ys > FW<W>::kMask) ++ys;
+    while (q > 0 && (uint64_t)(q - 1) >> ys > FW<W>::kMask) ++ys;
+    // q unset: buckets over a speculative range from a prefix, resolved on
+    // the device into qs (the kernels read it; ys / ybase above are unused).
+    const int2* qs = nullptr;
+    if (SPEC) {
+        const uint32_t np = (uint32_t)ctx->sm_count;
+        int rc0 = chp_ensure(ctx, ctx->yrange, (size_t)(np + 1) * sizeof(int2));
+        if (rc0) return rc0;
+        int2* part = (int2*)ctx->yrange.p;
+        k_yrange<<<np, 1024, 0, ctx->stream>>>(d_xy, std::min<uint64_t>(n, 1ull << 18), g, part);
+        CHP_LAUNCHED(ctx);
+        k_quant_shift<<<1, 32, 0, ctx->stream>>>(part, np, g, FW<W>::kMask, part + np);
+        CHP_LAUNCHED(ctx);
+        qs = part + np;
+    }
     uint32_t gshift = 0;
     while ((((uint64_t)(w + (1u << gshift) - 1) >> gshift) + 1) * sizeof(W) > fbudget) ++gshift;
     const uint32_t ngroups = (w + (1u << gshift) - 1) >> gshift;
@@ -1296,19 +1358,21 @@ int run_group_filter(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, const Geo& g
     auto pass = [&](const int32_t* xy, uint64_t cnt, const W* F) {
         const bool rf = force_read || (!force_red && cur_done < read_until);
         if (rf && !pl.tma) {
-            auto fn = k_reduce_filter<W, true, false>;
+            auto fn = k_reduce_filter<W, true, false, SPEC>;
             CHP_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
             int per_sm = 0;
             CHP_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreadsRF, pl.smem));
             fn<<<std::max(1, std::min(per_sm, 2)) * ctx->sm_count, kThreadsRF, pl.smem, ctx->stream>>>(
-                xy, cnt, g, w, gshift, ys, F, ngroups, pl.stages, d_L);
+                xy, cnt, g, w, gshift, ys, F, ngroups, pl.stages, d_L, qs);
             CHP_LAUNCHED(ctx);
         } else if (rf)
-            CHP_LAUNCH_PLANNED(ctx, pl, (k_reduce_filter<W, true, true>), (k_reduce_filter<W, true, false>), xy, cnt,
-                               g, w, gshift, ys, F, ngroups, pl.stages, d_L);
+            CHP_LAUNCH_PLANNED(ctx, pl, (k_reduce_filter<W, true, true, SPEC>), (k_reduce_filter<W, true, false, SPEC>),
+                               xy, cnt,
+                               g, w, gshift, ys, F, ngroups, pl.stages, d_L, qs);
         else
-            CHP_LAUNCH_PLANNED(ctx, pl, (k_reduce_filter<W, false, true>), (k_reduce_filter<W, false, false>), xy,
-                               cnt, g, w, gshift, ys, F, ngroups, pl.stages, d_L);
+            CHP_LAUNCH_PLANNED(ctx, pl, (k_reduce_filter<W, false, true, SPEC>),
+                               (k_reduce_filter<W, false, false, SPEC>), xy,
+                               cnt, g, w, gshift, ys, F, ngroups, pl.stages, d_L, qs);
         return CHP_OK;
     };
     // Phases double in length: warm-up n/2^kw (default n/64) with an empty
@@ -1324,7 +1388,7 @@ int run_group_filter(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, const Geo& g
     if ((rc = pass(d_xy, warm, nullptr))) return rc;
     for (uint64_t done = warm; done < n;) {
         k_filter_build<W><<<(ngroups + 1 + 255) / 256, 256, 0, ctx->stream>>>(d_L, w, gshift, (int32_t)g.ybase,
-                                                                            ys, (W*)ctx->filter.p, ngroups);
+                                                                            ys, (W*)ctx->filter.p, ngroups, qs);
         CHP_LAUNCHED(ctx);
         const uint64_t stop = std::min<uint64_t>(n, 2 * done);
         cur_done = done;
@@ -1393,7 +1457,7 @@ int chp_reduce_yr(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t width, 
     // speculative range from a prefix instead (Quant, k_yrange).
     const bool yspec = validate && q < 0 && ybase >= 0;
     const bool fits_sampled = (yknown || yspec) && g.wcheck == w && (size_t)wpad8 * 2 <= budget;
-    const bool fits_filter = yknown && g.wcheck == w;  // invalid x must clamp onto the sink
+    const bool fits_filter = (yknown || yspec) && g.wcheck == w;  // invalid x must clamp onto the sink
 
     enum { V_GLOBAL, V_SMEM32, V_SMEM16, V_FILTER8, V_FILTER, V_SAMPLED } v;
     if (flags & CHP_REDUCE_FORCE_GLOBAL) v = V_GLOBAL;
@@ -1587,11 +1651,14 @@ int chp_reduce_yr(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t width, 
             const size_t fbudget = (flags & CHP_REDUCE_FILTER_SMALL) ? 100 * 1024 : budget;
             int rc;
             if (flags & CHP_REDUCE_FILTER16)
-                rc = run_group_filter<uint32_t>(ctx, d_xy, n, g, w, q, flags, fbudget, d_L);
+                rc = yknown ? run_group_filter<uint32_t, false>(ctx, d_xy, n, g, w, q, flags, fbudget, d_L)
+                            : run_group_filter<uint32_t, true>(ctx, d_xy, n, g, w, q, flags, fbudget, d_L);
             else
-                rc = run_group_filter<uint16_t>(ctx, d_xy, n, g, w, q, flags, fbudget, d_L);
+                rc = yknown ? run_group_filter<uint16_t, false>(ctx, d_xy, n, g, w, q, flags, fbudget, d_L)
+                            : run_group_filter<uint16_t, true>(ctx, d_xy, n, g, w, q, flags, fbudget, d_L);
             if (rc) return rc;
-            ctx->variant = (flags & CHP_REDUCE_FILTER16) ? "filter16" : "filter";
+            ctx->variant = (flags & CHP_REDUCE_FILTER16) ? (yknown ? "filter16" : "filter16-yspec")
+                                                         : (yknown ? "filter" : "filter-yspec");
             return CHP_OK;
         }
         default: {

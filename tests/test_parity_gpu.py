@@ -157,13 +157,15 @@ def test_large_y_without_q(ctx, orc):
         check_against_oracle(orc, got, xy, 3, None)
 
 
+@pytest.mark.parametrize("p", [65536, 1 << 20])
 @pytest.mark.parametrize("case", ["narrow_prefix", "sorted_desc", "gaussian"])
-def test_q_unset_speculative_range(ctx, orc, case):
+def test_q_unset_speculative_range(ctx, orc, case, p):
     """q unset with a width beyond the smem tables: the sampled filter
-    quantises the y range of the first 2^18 points; points outside it (both
-    sides, far) must still be exact, and an invalid y must still fail."""
+    (p = 2^16) or the group filter (p = 2^20) quantises the y range of the
+    first 2^18 points; points outside it (both sides, far) must still be
+    exact, and an invalid y must still fail."""
     rng = np.random.default_rng(77)
-    p, n = 65536, 3_000_000
+    n = 3_000_000 if p == 65536 else 6_000_000  # (the group filter phases start at 4 Mi points)
     x = rng.integers(1, p + 1, size=n)
     if case == "narrow_prefix":
         y = rng.integers(1000, 2000, size=n)
@@ -175,7 +177,8 @@ def test_q_unset_speculative_range(ctx, orc, case):
         y = np.clip(np.rint(rng.normal(p / 2, p / 8, size=n)), 1, p)
     xy = np.stack([x, y], axis=1).astype(np.int32)
     got = run_device(ctx, xy, p, None)
-    assert ctx.variant.startswith("sampled") and ctx.variant.endswith("yspec"), ctx.variant
+    assert ctx.variant.startswith("sampled" if p == 65536 else "filter") and ctx.variant.endswith("yspec"), \
+        ctx.variant
     check_against_oracle(orc, got, xy, p, None)
     bad = xy.copy()
     bad[n - 5] = (7, 0)
