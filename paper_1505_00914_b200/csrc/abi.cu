@@ -6,6 +6,7 @@
 // previous chunk on the compute stream (two device buffers, event-ordered),
 // then K3 (+K4) run on device and only L / the chain / the hull come back.
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <condition_variable>
 #include <cstdlib>
@@ -20,9 +21,12 @@
 
 namespace {
 
-// Persistent host workers for the packed pipeline: run(f) calls f(i) for
-// i in [0, parts) on the workers and the caller, and returns when all are
-// done.  One job at a time (the pipeline is single-threaded per context).
+// Persistent host workers for the packed pipeline: run(f, k) calls f(i) for
+// i in [0, k) on the workers and the caller, and returns when all are done.
+// One job at a time (the pipeline is single-threaded per context).  Only the
+// k - 1 workers a job uses are waited for, and a worker spins briefly on the
+// job counter before sleeping, so back-to-back calls (a chunk loop, or a
+// caller timing 0.2-1 ms calls) do not pay a futex wake-up per worker.
 class HostPool {
   public:
     explicit HostPool(int workers) {
@@ -31,14 +35,14 @@ class HostPool {
     ~HostPool() {
         {
             std::lock_guard<std::mutex> g(m_);
-            stop_ = true;
+            stop_.store(true);
         }
         cv_.notify_all();
         for (auto& t : th_) t.join();
     }
     int parts() const { return (int)th_.size() + 1; }
     // Parts worth waking for m items (>= 32 Ki each): small host calls stay
-    // on the caller's thread instead of paying 15 wake-ups and their jitter.
+    // on the caller's thread.
     int parts_for(uint64_t m) const {
         const uint64_t k = (m + (32u << 10) - 1) / (32u << 10);
         return (int)std::max<uint64_t>(1, std::min<uint64_t>(k, (uint64_t)parts()));
@@ -50,17 +54,26 @@ class HostPool {
             f(0);
             return;
         }
+        job_ = &f;
+        pending_.store(k - 1);
         {
+            // generation and part count in one word, so a worker that wakes
+            // late never pairs one job's generation with another's count
             std::lock_guard<std::mutex> g(m_);
-            job_ = &f;
-            active_ = k;
-            pending_ = (int)th_.size();
-            ++gen_;
+            const uint64_t gen = (gen_.load(std::memory_order_relaxed) >> 8) + 1;
+            gen_.store((gen << 8) | (uint64_t)k, std::memory_order_release);
         }
         cv_.notify_all();
         f(0);
-        std::unique_lock<std::mutex> lk(m_);
-        done_.wait(lk, [this] { return pending_ == 0; });
+        const auto t0 = std::chrono::steady_clock::now();
+        while (pending_.load(std::memory_order_acquire) != 0) {
+            if (std::chrono::steady_clock::now() - t0 > std::chrono::microseconds(200)) {
+                std::unique_lock<std::mutex> lk(m_);
+                done_.wait(lk, [this] { return pending_.load() == 0; });
+                break;
+            }
+            _mm_pause();
+        }
         job_ = nullptr;
     }
 
@@ -68,19 +81,22 @@ class HostPool {
     void loop(int id) {
         uint64_t seen = 0;
         for (;;) {
-            const std::function<void(int)>* job;
-            {
+            // Spin up to ~0.5 ms for the next job, then sleep.
+            const auto t0 = std::chrono::steady_clock::now();
+            while (gen_.load(std::memory_order_acquire) == seen && !stop_.load(std::memory_order_relaxed) &&
+                   std::chrono::steady_clock::now() - t0 < std::chrono::microseconds(500))
+                _mm_pause();
+            if (gen_.load(std::memory_order_acquire) == seen) {
                 std::unique_lock<std::mutex> lk(m_);
-                cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
-                if (stop_) return;
-                seen = gen_;
-                job = job_;
-                if (id >= active_) job = nullptr;
+                cv_.wait(lk, [&] { return stop_.load() || gen_.load() != seen; });
             }
-            if (job) (*job)(id);
-            {
+            if (stop_.load()) return;
+            seen = gen_.load(std::memory_order_acquire);
+            if (id >= (int)(seen & 0xFF)) continue;  // not part of this job
+            (*job_)(id);
+            if (pending_.fetch_sub(1, std::memory_order_acq_rel) == 1) {
                 std::lock_guard<std::mutex> g(m_);
-                if (--pending_ == 0) done_.notify_one();
+                done_.notify_one();
             }
         }
     }
@@ -88,9 +104,9 @@ class HostPool {
     std::mutex m_;
     std::condition_variable cv_, done_;
     const std::function<void(int)>* job_ = nullptr;
-    uint64_t gen_ = 0;
-    int pending_ = 0, active_ = 0;
-    bool stop_ = false;
+    std::atomic<uint64_t> gen_{0};  // (generation << 8) | parts of the current job
+    std::atomic<int> pending_{0};
+    std::atomic<bool> stop_{false};
 };
 
 HostPool* pool_of(chp_ctx* ctx) {
