@@ -90,19 +90,21 @@ uint64_t chp_dl_len(int64_t width);
 #define CHP_REDUCE_TMA 4096u        /* tuning: stream via the TMA bulk-copy ring */
 #define CHP_REDUCE_FORCE_SAMPLED 8192u /* testing: force the sampled per-column filter */
 #define CHP_REDUCE_FUSED 16384u     /* tuning: sampled filter as 1 cooperative kernel (grid barriers) */
-#define CHP_REDUCE_SAMPLE_K(k) ((uint32_t)(k) << 16) /* tuning: sample n/2^k (k in 1..7, default 4) */
-/* bits 19-21: group-filter phase-A fraction n/2^ka (default 3) */
+#define CHP_REDUCE_SAMPLE_K(k) ((uint32_t)(k) << 16) /* tuning (k in 1..7): the sampled filter samples n/2^k
+                                                         (default 4); the group filter warms up on n/2^(k+3)
+                                                         (default 6) */
 #define CHP_REDUCE_SAMPLE_TMA (1u << 22) /* tuning: sample pass streams through the TMA ring */
-#define CHP_PIPELINE_NO_PACK (1u << 23) /* host pipelines: always send int32 pairs (no 16-bit packing) */
+#define CHP_PIPELINE_NO_PACK (1u << 23) /* host pipelines: always send int32 pairs (no 16/42-bit packing) */
 #define CHP_REDUCE_SAMPLE_SPLIT (1u << 25) /* tuning: sampled filter's sample pass and merge as separate launches */
 #define CHP_REDUCE_BLOCKED (1u << 26) /* tuning: smem/filter streams in per-CTA contiguous slices (the sampled main pass always is) */
 #define CHP_REDUCE_SAMPLE_PREFIX (1u << 27) /* tuning: sampled filter samples the first n/2^k points (default: the head of each CTA slice) */
 
 /* Algorithm 1 over n int32 (x,y) pairs at d_xy (8-byte aligned).  Slot of a
  * point is x - x_off - 1; a point is valid when that slot is in [0,width)
- * and (unless NO_VALIDATE) 1 <= y <= q (q < 0: no upper bound).  Invalid
- * points are skipped and flagged in d_L's error word; chp_check() turns the
- * flag into CHP_EINVAL.  Asynchronous. */
+ * and (unless NO_VALIDATE) 1 <= y <= q (q < 0: no upper bound; the filter
+ * variants then bucket a y range taken from a prefix, exact for any y).
+ * Invalid points are skipped and flagged in d_L's error word; chp_check()
+ * turns the flag into CHP_EINVAL.  Asynchronous (no host synchronisation). */
 int chp_reduce(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t width,
                int64_t q, int64_t x_off, int32_t* d_L, uint32_t flags);
 
