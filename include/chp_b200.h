@@ -15,21 +15,21 @@
  * Reference interfaces each entry point replaces (paths under
  * /root/reference/proj):
  *   chp_reduce            chp::reducer::reduce          include/chp/reducer.hpp:65-67,
- *                                                       src/reducer.cpp:172-182 (+ bucket :122-135)
- *   chp_compact           chp::reducer::build_polyline  include/chp/reducer.hpp:76, src/reducer.cpp:211-222;
- *                         ExtremalArray::valid_count    src/reducer.cpp:145-152;
+ *                                                       src/reducer.cpp:69-79 (+ bucket :19-32)
+ *   chp_compact           chp::reducer::build_polyline  include/chp/reducer.hpp:76, src/reducer.cpp:108-119;
+ *                         ExtremalArray::valid_count    src/reducer.cpp:42-49;
  *                         occupancy::BlockedBitset words include/chp/occupancy.hpp:58-109;
- *                         serialize's (width+1,-1) form  src/reducer.cpp:224-233
+ *                         serialize's (width+1,-1) form  src/reducer.cpp:121-130
  *   chp_ns_chain          the north_star chain order (no reference function)
- *   chp_hull              chp::hulls::melkman           include/chp/hulls.hpp:24, src/hulls.cpp:396-440
- *                         + canonicalize_hull           src/geometry.cpp:407-445
- *   chp_bounds            chp::kernels::min_max         include/chp/kernels.hpp:33, src/kernels.cpp:580-583
- *   chp_translate         chp::kernels::translate       include/chp/kernels.hpp:34-35, src/kernels.cpp:585-590
+ *   chp_hull              chp::hulls::melkman           include/chp/hulls.hpp:24, src/hulls.cpp:137-181
+ *                         + canonicalize_hull           src/geometry.cpp:42-80
+ *   chp_bounds            chp::kernels::min_max         include/chp/kernels.hpp:33, src/kernels.cpp:55-58
+ *   chp_translate         chp::kernels::translate       include/chp/kernels.hpp:34-35, src/kernels.cpp:60-65
  *   chp_pipeline_host     reduce + build_polyline (+ melkman) from HOST buffers, the drop-in's
- *                         workhorse (src/reducer.cpp:172-182, :211-222; src/hulls.cpp:396-440)
+ *                         workhorse (src/reducer.cpp:69-79, :108-119; src/hulls.cpp:137-181)
  *   chp_precondition_host chp::reducer::precondition    include/chp/reducer.hpp:100-101,
  *   chp_precondition_run  (one-pass form of the above, outputs via chp_last_outputs)
- *                                                       src/reducer.cpp:235-281
+ *                                                       src/reducer.cpp:132-178
  */
 #ifndef CHP_B200_H
 #define CHP_B200_H
@@ -119,7 +119,7 @@ int chp_dl_from_pairs(chp_ctx* ctx, const int32_t* d_Lpairs, int64_t width,
 
 /* Synchronise and read d_L's error word: CHP_EINVAL if an invalid
  * coordinate was seen (reference: std::invalid_argument,
- * src/reducer.cpp:175-178). */
+ * src/reducer.cpp:72-75). */
 int chp_check(chp_ctx* ctx, const int32_t* d_L, int64_t width);
 
 /* ------------------------------------------------------ K3: compaction
@@ -184,12 +184,12 @@ int chp_pipeline_host(chp_ctx* ctx, const int32_t* h_xy, uint64_t n,
 /* build_polyline / valid_count of a HOST L in serialize form (h_Lpairs,
  * empty slots any lo > hi) with ExtremalArray's offsets: uploads L, K3 on
  * device, chain back.  h_chain holds 2*width points.  CHP_EINVAL when no
- * slot is valid and h_chain is requested (src/reducer.cpp:219-220). */
+ * slot is valid and h_chain is requested (src/reducer.cpp:116-117). */
 int chp_polyline_host(chp_ctx* ctx, const int32_t* h_Lpairs, int64_t width,
                       int64_t major_off, int64_t minor_off, int swapped,
                       int32_t* h_chain, int64_t* h_s);
 
-/* precondition (x-only mode, src/reducer.cpp:235-281): bounds, width =
+/* precondition (x-only mode, src/reducer.cpp:132-178): bounds, width =
  * x_max-x_min+1, fold with x_off = x_min-1 and y untranslated, Lemma-1
  * chain.  h_bbox4 = {x_min,x_max,y_min,y_max}.  The chain buffer must hold
  * 2*width points: call with h_chain == NULL first to learn width via

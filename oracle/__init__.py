@@ -92,7 +92,7 @@ class Oracle:
 
     # -- reduction
     def reduce(self, points, width: int, q: int | None = None):
-        """reducer::reduce (src/reducer.cpp:172-182). Returns a dict with
+        """reducer::reduce (src/reducer.cpp:69-79). Returns a dict with
         lo, hi, valid, occ; raises ValueError where the reference throws
         std::invalid_argument."""
         xy = _xy(points)
@@ -160,7 +160,7 @@ class Oracle:
         return tuple(int(v) for v in out)
 
     def precondition(self, points):
-        """reducer::precondition, x-only mode (src/reducer.cpp:235-281):
+        """reducer::precondition, x-only mode (src/reducer.cpp:132-178):
         bounds, width = x_max - x_min + 1, bucket with x_off = x_min - 1 and
         y untranslated, Lemma-1 chain, Melkman hull."""
         xy = _xy(points)

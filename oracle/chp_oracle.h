@@ -34,7 +34,7 @@ uint64_t or_fnv1a64(const void* data, size_t len);
  * before y, :59).  Writes n interleaved int32 (x,y) pairs. */
 void or_gen_uniform_box(uint64_t n, int64_t p, uint64_t seed, int32_t* xy);
 
-/* reducer::reduce, src/reducer.cpp:172-182: validation pass (:175-178) then
+/* reducer::reduce, src/reducer.cpp:69-79: validation pass (:72-75) then
  * the Algorithm-1 fold `bucket` (:122-135).  lo/hi/valid have `width`
  * entries, occ has ceil(width/64) words in BlockedBitset<uint64_t> layout
  * (include/chp/occupancy.hpp:46-49, :70-74).  q < 0 means "no q".
@@ -44,25 +44,25 @@ int or_reduce(const int32_t* xy, uint64_t n, int64_t width, int64_t q,
 
 /* The fold alone on pre-translated points (no validation), accumulating
  * into existing arrays: bucket() with slot = x - x_off - 1
- * (src/reducer.cpp:122-135, translation as in :263-271). */
+ * (src/reducer.cpp:19-32, translation as in :160-168). */
 void or_bucket(const int32_t* xy, uint64_t n, int64_t x_off, int32_t* lo,
                int32_t* hi, uint8_t* valid, uint64_t* occ);
 
 /* L in int32 (lo,hi) pairs, empty slots as the (width+1,-1) sentinel of
- * serialize(), src/reducer.cpp:224-233. */
+ * serialize(), src/reducer.cpp:121-130. */
 void or_L_pairs(int64_t width, const int32_t* lo, const int32_t* hi,
                 const uint8_t* valid, int32_t* out_pairs);
 
-/* serialize() text, src/reducer.cpp:224-233.  Returns bytes written (or
+/* serialize() text, src/reducer.cpp:121-130.  Returns bytes written (or
  * needed, when buf is NULL). */
 size_t or_serialize(int64_t width, const int32_t* lo, const int32_t* hi,
                     const uint8_t* valid, char* buf, size_t cap);
 
-/* ExtremalArray::valid_count, src/reducer.cpp:145-152. */
+/* ExtremalArray::valid_count, src/reducer.cpp:42-49. */
 int64_t or_valid_count(int64_t width, const int32_t* lo, const int32_t* hi,
                        const uint64_t* occ);
 
-/* build_polyline, src/reducer.cpp:211-222: ctz walk of the occupancy words
+/* build_polyline, src/reducer.cpp:108-119: ctz walk of the occupancy words
  * (include/chp/occupancy.hpp:83-93) emitting to_original(i,lo) then
  * to_original(i,hi) when hi != lo (include/chp/reducer.hpp:46-50).
  * Returns the chain length s, or -1 when empty (reference throws). */
@@ -76,19 +76,19 @@ int64_t or_build_polyline(int64_t width, const int32_t* lo, const int32_t* hi,
 int64_t or_ns_chain(int64_t width, const int32_t* lo, const int32_t* hi,
                     const uint64_t* occ, int64_t major_off, int32_t* chain_xy);
 
-/* hulls::melkman, src/hulls.cpp:396-440, finished by canonicalize_hull,
- * src/geometry.cpp:407-445.  Returns h, or -1 on empty input. */
+/* hulls::melkman, src/hulls.cpp:137-181, finished by canonicalize_hull,
+ * src/geometry.cpp:42-80.  Returns h, or -1 on empty input. */
 int64_t or_melkman(const int32_t* chain_xy, int64_t s, int32_t* hull_xy);
 
-/* canonicalize_hull, src/geometry.cpp:407-445 (in/out may not alias). */
+/* canonicalize_hull, src/geometry.cpp:42-80 (in/out may not alias). */
 int64_t or_canonicalize(const int32_t* v_xy, int64_t m, int32_t* hull_xy);
 
 /* Andrew monotone chain on the lex-sorted unique points, strict, CCW from
  * the lex-min vertex -- an independent cross-check of or_melkman (equal to
- * graham_scan, src/hulls.cpp:293-320, on every input). */
+ * graham_scan, src/hulls.cpp:34-61, on every input). */
 int64_t or_monotone_hull(const int32_t* xy, int64_t n, int32_t* hull_xy);
 
-/* kernels::min_max_scalar, src/kernels.cpp:533-542. n >= 1. */
+/* kernels::min_max_scalar, src/kernels.cpp:8-17. n >= 1. */
 void or_min_max(const int32_t* xy, uint64_t n, int64_t out4[4]);
 
 #ifdef __cplusplus

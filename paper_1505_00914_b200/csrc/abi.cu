@@ -916,7 +916,7 @@ static int precondition_core(chp_ctx* ctx, const HostPts& in, uint64_t n, int64_
     const int64_t width = (int64_t)b4[1] - b4[0] + 1;
     if (bounds_only) return CHP_OK;
     if (width > (1ll << 29)) return chp_einval(ctx, "precondition: x extent exceeds the device limit 2^29");
-    const int64_t x_off = (int64_t)b4[0] - 1;  // major_offset, src/reducer.cpp:258
+    const int64_t x_off = (int64_t)b4[0] - 1;  // major_offset, src/reducer.cpp:154
     if ((rc = chp_ensure(ctx, ctx->dl, chp_dl_len(width) * 4))) return rc;
     // Every point lies in the bounding box, so K1 runs with the box's y range
     // as the valid range: the filter variants (and, streamed, the 16-bit

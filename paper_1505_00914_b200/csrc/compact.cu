@@ -1,9 +1,9 @@
 // compact.cu -- K3: skip-invalid compaction of L into the ordered chain.
 //
-// Replaces build_polyline (/root/reference/proj/src/reducer.cpp:211-222),
+// Replaces build_polyline (/root/reference/proj/src/reducer.cpp:108-119),
 // the ctz walk of the occupancy words it iterates
 // (include/chp/occupancy.hpp:83-93), ExtremalArray::valid_count
-// (src/reducer.cpp:145-152) and serialize's (width+1,-1) form (:224-233).
+// (src/reducer.cpp:42-49) and serialize's (width+1,-1) form (:121-130).
 //
 // One pass over the 8-byte slots with a single-pass decoupled look-back scan
 // (tiles of 2048 slots, 256 threads x 8 slots, dynamic tile order so every

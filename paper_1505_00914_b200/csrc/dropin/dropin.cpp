@@ -5,13 +5,13 @@
 // occupancy words, chain or hull into the reference's value types.
 //
 // Reference behaviour reproduced (paths under /root/reference/proj):
-//   reduce          src/reducer.cpp:172-182   width/coordinate checks -> invalid_argument
-//   build_polyline  src/reducer.cpp:211-222   empty -> invalid_argument
-//   serialize       src/reducer.cpp:224-233
-//   second_scan     src/reducer.cpp:184-209
-//   precondition    src/reducer.cpp:235-281   (x-only, auto_axis, second_scan)
-//   melkman & co.   src/hulls.cpp:293-483     canonical Hull, input checks
-//   min_max etc.    src/kernels.cpp:533-592
+//   reduce          src/reducer.cpp:69-79   width/coordinate checks -> invalid_argument
+//   build_polyline  src/reducer.cpp:108-119   empty -> invalid_argument
+//   serialize       src/reducer.cpp:121-130
+//   second_scan     src/reducer.cpp:81-106
+//   precondition    src/reducer.cpp:132-178   (x-only, auto_axis, second_scan)
+//   melkman & co.   src/hulls.cpp:34-224     canonical Hull, input checks
+//   min_max etc.    src/kernels.cpp:8-67
 #include <algorithm>
 #include <chrono>
 #include <cstdlib>

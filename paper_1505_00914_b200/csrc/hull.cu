@@ -1,7 +1,7 @@
 // hull.cu -- K4: exact convex hull of the reduced set, on device.
 //
 // Replaces hulls::melkman + canonicalize_hull
-// (/root/reference/proj/src/hulls.cpp:396-440, src/geometry.cpp:407-445) for
+// (/root/reference/proj/src/hulls.cpp:137-181, src/geometry.cpp:42-80) for
 // chains produced by the reduction.  Melkman's deque is inherently serial
 // (53-66 ns per chain point on a CPU core) and, run on the
 // north_star order, wrong for single-point columns (F3).  Here the hull is
@@ -25,7 +25,7 @@
 //   final  : one CTA stitches lower ++ upper (dropping the shared end
 //            points of single-point extreme columns), which is already CCW
 //            from the lexicographic minimum; degenerate sets come out as
-//            1 or 2 vertices {lexmin, lexmax} as in src/geometry.cpp:394-403.
+//            1 or 2 vertices {lexmin, lexmax} as in src/geometry.cpp:29-38.
 // With cooperative launch the three stages are ONE kernel (a grid barrier
 // per merge level); otherwise one launch per stage and level.
 // Orientation tests are exact (__int128 cross products,

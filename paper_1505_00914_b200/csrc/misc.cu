@@ -1,9 +1,9 @@
 // misc.cu -- K0 bounds, translation and the synthetic workload generators.
 //
 // chp_bounds replaces kernels::min_max / min_max_avx2
-// (/root/reference/proj/src/kernels.cpp:580-583, src/kernels_avx2.cpp:25-53):
+// (/root/reference/proj/src/kernels.cpp:55-58, src/kernels_avx2.cpp:25-53):
 // one streaming pass, warp shuffles, one atomic per warp.  chp_translate
-// replaces kernels::translate (src/kernels.cpp:585-590); on the hot path the
+// replaces kernels::translate (src/kernels.cpp:60-65); on the hot path the
 // translation is fused into K1's slot computation instead (x_off).
 #include <algorithm>
 #include <thread>

@@ -1,7 +1,7 @@
 // reduce.cu -- K1: Algorithm 1 (per-x-column min/max of y) on sm_100a.
 //
 // Replaces reducer::reduce's validation pass and the bucket() fold
-// (/root/reference/proj/src/reducer.cpp:172-182, :122-135).  The fold is a
+// (/root/reference/proj/src/reducer.cpp:69-79, :19-32).  The fold is a
 // scatter-min over a p-slot table, so the kernel is HBM-bound on the 8-byte
 // point stream when every per-point table access stays on chip:
 //

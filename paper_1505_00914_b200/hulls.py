@@ -1,7 +1,7 @@
 """Python mirror of chp::hulls::melkman (/root/reference/proj/include/chp/hulls.hpp:24)
 backed by the device hull (K4).
 
-The reference runs Melkman's deque over the chain (src/hulls.cpp:396-440).
+The reference runs Melkman's deque over the chain (src/hulls.cpp:137-181).
 Here the chain's points are re-reduced on the device (bounds, Algorithm 1,
 compaction -- exact by the reducer's idempotence) and the hull is the
 multi-level monotone chain of csrc/hull.cu.  For every simple chain (every
@@ -34,7 +34,7 @@ class Hull:
 
 
 def melkman(chain: PolygonalChain) -> Hull:
-    """ValueError on an empty chain (src/hulls.cpp:398)."""
+    """ValueError on an empty chain (src/hulls.cpp:139)."""
     pts = chain.vertices if isinstance(chain, PolygonalChain) else chain
     xy = _as_int32_points(pts)
     if len(xy) == 0:

@@ -21,7 +21,7 @@ class MinMax:
 
 
 def min_max(points) -> MinMax:
-    """ValueError on empty input (src/kernels.cpp:580-583)."""
+    """ValueError on empty input (src/kernels.cpp:55-58)."""
     xy = _as_int32_points(points)
     if len(xy) == 0:
         raise ValueError("min_max: empty input")
@@ -36,7 +36,7 @@ def find_bounds(points) -> BoundingBox:
 
 
 def translate(points, dx: int, dy: int) -> np.ndarray:
-    """out[i] = in[i] + (dx, dy) on the device (src/kernels.cpp:585-590)."""
+    """out[i] = in[i] + (dx, dy) on the device (src/kernels.cpp:60-65)."""
     xy = _as_int32_points(points)
     if len(xy) == 0:
         return xy.copy()

@@ -107,7 +107,7 @@ class ExtremalArray:
         return self._chain
 
     def valid_count(self) -> int:
-        """reducer.cpp:145-152"""
+        """reducer.cpp:42-49"""
         return int(len(self._device_chain()))
 
     def valid_points(self) -> np.ndarray:
@@ -116,7 +116,7 @@ class ExtremalArray:
 
 
 def reduce(points, width: int, q: int | None = None, occ_kind: Kind = Kind.array) -> ExtremalArray:
-    """Algorithm 1 on the device (src/reducer.cpp:172-182).  Raises
+    """Algorithm 1 on the device (src/reducer.cpp:69-79).  Raises
     ValueError for width < 1 or any coordinate outside x in [1,width],
     y >= 1 (y <= q when q is given)."""
     if int(width) < 1:
@@ -128,7 +128,7 @@ def reduce(points, width: int, q: int | None = None, occ_kind: Kind = Kind.array
 
 
 def build_polyline(arr: ExtremalArray) -> PolygonalChain:
-    """Lemma-1 chain (src/reducer.cpp:211-222); ValueError when empty."""
+    """Lemma-1 chain (src/reducer.cpp:108-119); ValueError when empty."""
     chain = arr._device_chain()
     if len(chain) == 0:
         raise ValueError("build_polyline: no valid points")
@@ -137,7 +137,7 @@ def build_polyline(arr: ExtremalArray) -> PolygonalChain:
 
 def serialize(arr: ExtremalArray, os: io.TextIOBase | None = None) -> str:
     """One line per slot, "i lo hi", empty slots "i <width+1> -1"
-    (src/reducer.cpp:224-233)."""
+    (src/reducer.cpp:121-130)."""
     lines = [f"{i} {lo} {hi}\n" for i, (lo, hi) in enumerate(arr.pairs.tolist(), start=1)]
     w1 = arr.width() + 1
     v = arr.valid.tolist()
@@ -170,7 +170,7 @@ class PreconditionResult:
 
 
 def precondition(points, options: PreconditionOptions | None = None) -> PreconditionResult:
-    """Steps 1-3 on the device (src/reducer.cpp:235-281), x-only mode:
+    """Steps 1-3 on the device (src/reducer.cpp:132-178), x-only mode:
     bounds, fold with x_off = x_min - 1 and y untranslated, Lemma-1 chain."""
     import time
 
@@ -187,7 +187,7 @@ def precondition(points, options: PreconditionOptions | None = None) -> Precondi
     t1 = time.perf_counter()
     res = ctx.precondition_host(xy[:, ::-1].copy() if swap else xy, chain=True)
     # Device L stores untranslated minor values; translate them when the
-    # reference does (full_bounds: src/reducer.cpp:259-261).
+    # reference does (full_bounds: src/reducer.cpp:156-158).
     minor_off = ((x_min if swap else y_min) - 1) if full_bounds else 0
     pairs = res["L"].astype(np.int64)
     valid = pairs[:, 0] <= pairs[:, 1]
@@ -206,7 +206,7 @@ def precondition(points, options: PreconditionOptions | None = None) -> Precondi
 
 
 def second_scan(arr: ExtremalArray, occ_kind: Kind = Kind.array) -> ExtremalArray:
-    """Re-bucket the survivors along the other axis (src/reducer.cpp:184-209):
+    """Re-bucket the survivors along the other axis (src/reducer.cpp:81-106):
     the <= 2w survivors are re-reduced on the device with axes swapped."""
     pts = arr.valid_points().astype(np.int64)
     swapped = not arr.axis_swapped
@@ -227,7 +227,7 @@ def second_scan(arr: ExtremalArray, occ_kind: Kind = Kind.array) -> ExtremalArra
 
 
 def translate(points, bbox: BoundingBox) -> np.ndarray:
-    """src/reducer.cpp:165-170 on the device."""
+    """src/reducer.cpp:62-67 on the device."""
     from .kernels import translate as ktranslate
 
     xy = _as_int32_points(points)

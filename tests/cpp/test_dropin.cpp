@@ -192,7 +192,7 @@ void reducer_kats() {
 
 void hull_kats() {
     using namespace chp::hulls;
-    // test_hulls.cpp:327-370
+    // test_hulls.cpp:13-56
     const std::vector<Point> sq{{0, 0}, {4, 0}, {4, 4}, {0, 4}, {2, 2}};
     const Hull sqh{{{0, 0}, {4, 0}, {4, 4}, {0, 4}}};
     EXPECT(graham_scan(sq) == sqh && quickhull(sq) == sqh && jarvis_march(sq) == sqh && brute_force_hull(sq) == sqh);

@@ -61,7 +61,7 @@ def test_reducer_kats(orc):
 
 
 def test_hull_kats(orc):
-    # test_hulls.cpp:418-442
+    # test_hulls.cpp:104-128
     assert orc.melkman([(0, 0), (4, 0), (2, 3)]).tolist() == [[0, 0], [4, 0], [2, 3]]
     stair = [(i + d, i) for i in range(10) for d in (0, 1)]
     assert np.array_equal(orc.melkman(stair), orc.monotone_hull(stair))
@@ -69,7 +69,7 @@ def test_hull_kats(orc):
     assert orc.melkman([(0, 0), (2, 2), (5, 5)]).tolist() == [[0, 0], [5, 5]]
     with pytest.raises(ValueError):
         orc.melkman(np.empty((0, 2), np.int32))
-    # canonicalize (src/geometry.cpp:407-445)
+    # canonicalize (src/geometry.cpp:42-80)
     # clockwise, a collinear vertex, a duplicate -> CCW from the lex-min vertex
     assert orc.canonicalize([(0, 4), (4, 4), (4, 0), (2, 0), (2, 0), (0, 0)]).tolist() == [[0, 0], [4, 0], [4, 4],
                                                                                          [0, 4]]
