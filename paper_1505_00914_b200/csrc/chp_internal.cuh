@@ -151,8 +151,11 @@ __device__ __forceinline__ void grid_barrier(GridBar* b) {
         const unsigned long long old = atomicAdd(&b->count, 1ull);
         const unsigned long long target = old - old % G + G;
         unsigned long long cur;
+        // Relaxed polls (an acquire load invalidates L1 on every poll:
+        // CCTL.IVALL), then one fence that orders the reads after the
+        // barrier behind the observed arrivals.
         do {
-            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(cur) : "l"(&b->count) : "memory");
+            asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(cur) : "l"(&b->count) : "memory");
         } while (cur < target);
         __threadfence();
     }
