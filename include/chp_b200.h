@@ -27,6 +27,11 @@
  *   chp_translate         chp::kernels::translate       include/chp/kernels.hpp:34-35, src/kernels.cpp:60-65
  *   chp_pipeline_host     reduce + build_polyline (+ melkman) from HOST buffers, the drop-in's
  *                         workhorse (src/reducer.cpp:69-79, :108-119; src/hulls.cpp:137-181)
+ *   chp_reduce_host /     the two halves of chp_pipeline_host (reduce into a device L;
+ *   chp_finish_host       build_polyline + melkman of it), for cross-device combines
+ *   chp_reduce_sharded,   chp::reducer::reduce over G devices: no reference
+ *   chp_pipeline_host_sharded  counterpart (the reference is single-threaded); same L as
+ *                         src/reducer.cpp:69-79, merge law tests/test_reducer.cpp:113-127
  *   chp_precondition_host chp::reducer::precondition    include/chp/reducer.hpp:100-101,
  *   chp_precondition_run  (one-pass form of the above, outputs via chp_last_outputs)
  *                                                       src/reducer.cpp:132-178
@@ -189,6 +194,21 @@ int chp_polyline_host(chp_ctx* ctx, const int32_t* h_Lpairs, int64_t width,
                       int64_t major_off, int64_t minor_off, int swapped,
                       int32_t* h_chain, int64_t* h_s);
 
+/* The two halves of chp_pipeline_host, for callers that combine partial Ls
+ * across devices between them (bench.py's N > 1 e2e leg, shard groups):
+ * chp_reduce_host initialises the caller's device DL d_L and streams the
+ * HOST points into it (chunked H2D overlapped with K1, packed where the
+ * range allows); it returns once the host buffer is no longer read and d_L
+ * is complete, WITHOUT failing on an invalid coordinate (the error word
+ * travels in d_L, so it survives a MIN combine).  chp_finish_host compacts
+ * a device DL (K3, + K4 when a hull is requested) and copies the requested
+ * outputs to the host, CHP_EINVAL when the error word is set (as
+ * chp_pipeline_host).  Both synchronous. */
+int chp_reduce_host(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t width, int64_t q, int32_t* d_L);
+int chp_reduce_host64(chp_ctx* ctx, const int64_t* h_xy, uint64_t n, int64_t width, int64_t q, int32_t* d_L);
+int chp_finish_host(chp_ctx* ctx, const int32_t* d_L, int64_t width, int32_t* h_Lpairs, uint64_t* h_occ,
+                    int32_t* h_chain, int64_t* h_s, int32_t* h_hull, int64_t* h_h);
+
 /* precondition (x-only mode, src/reducer.cpp:132-178): bounds, width =
  * x_max-x_min+1, fold with x_off = x_min-1 and y untranslated, Lemma-1
  * chain.  h_bbox4 = {x_min,x_max,y_min,y_max}.  The chain buffer must hold
@@ -219,6 +239,48 @@ int chp_pipeline_host64(chp_ctx* ctx, const int64_t* h_xy, uint64_t n, int64_t w
 int chp_precondition_run64(chp_ctx* ctx, const int64_t* h_xy, uint64_t n, int swap_axes, int want_hull,
                            int64_t* h_bbox4, int64_t* h_width, int64_t* h_s, int64_t* h_h);
 int chp_bounds_host64(chp_ctx* ctx, const int64_t* h_xy, uint64_t n, int64_t* h_bbox4);
+
+/* ------------------------------------------- multi-GPU shard groups
+ * reduce over G devices of one box in ONE process: the
+ * points are split into contiguous equal slices (shard k owns
+ * [k n/G, (k+1) n/G)), each device folds its slice into a partial DL, and
+ * the partials meet in ONE element-wise MIN (storing ~hi makes every DL
+ * word a min; the error word merges too).  Exact for any partition: the
+ * same L as src/reducer.cpp:69-79 over all n points (min/max are
+ * associative and commutative, tests/test_reducer.cpp:113-127).
+ *   CHP_COMBINE_NCCL  ncclAllReduce(ncclInt32, ncclMin) over a communicator
+ *                     from ncclCommInitAll (distinct devices; libnccl.so.2
+ *                     is loaded on first use)
+ *   CHP_COMBINE_PEER  device 0 waits on every shard's K1 and one kernel
+ *                     reads the partial DLs over peer memory (NVLink P2P);
+ *                     devices may repeat (G contexts on one device). */
+#define CHP_COMBINE_NCCL 0
+#define CHP_COMBINE_PEER 1
+typedef struct chp_group chp_group;
+int chp_group_create(const int* devices, int G, int combine, chp_group** out);
+void chp_group_destroy(chp_group* g);
+/* The context of shard k (owned by the group; usable for single-device calls). */
+chp_ctx* chp_group_ctx(chp_group* g, int k);
+int chp_group_size(const chp_group* g);
+const char* chp_group_last_error(const chp_group* g);
+/* Host->device bytes of the last chp_pipeline_host*_sharded call, all shards. */
+uint64_t chp_group_last_h2d_bytes(const chp_group* g);
+/* Device-resident shards: d_xy[k] (n[k] points) on shard k's device.  On
+ * return (asynchronous, on the shards' context streams) d_L[0] holds the
+ * merged DL -- with CHP_COMBINE_NCCL every d_L[k] does.  Compact it with
+ * chp_compact on chp_group_ctx(g, 0). */
+int chp_reduce_sharded(chp_group* g, const int32_t* const* d_xy, const uint64_t* n, int64_t width, int64_t q,
+                       int32_t* const* d_L);
+/* chp_pipeline_host over the group: one host thread per shard streams its
+ * slice of the HOST input to its device, the partial DLs are combined, and
+ * K3 (+K4) run on shard 0; outputs and errors exactly as chp_pipeline_host
+ * (the int64 form as chp_pipeline_host64).  Synchronous. */
+int chp_pipeline_host_sharded(chp_group* g, const int32_t* h_xy, uint64_t n, int64_t width, int64_t q,
+                              int32_t* h_Lpairs, uint64_t* h_occ, int32_t* h_chain, int64_t* h_s,
+                              int32_t* h_hull, int64_t* h_h);
+int chp_pipeline_host64_sharded(chp_group* g, const int64_t* h_xy, uint64_t n, int64_t width, int64_t q,
+                                int32_t* h_Lpairs, uint64_t* h_occ, int32_t* h_chain, int64_t* h_s,
+                                int32_t* h_hull, int64_t* h_h);
 
 /* ------------------------------------------------- synthetic workloads
  * Deterministic, counter-based generators of the BASELINE.json configs

@@ -21,6 +21,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(HERE, "_build", "liboracle.so")
+GEN_SO = os.path.join(HERE, "_build", "libchpgen.so")
 REF_SO = os.path.join(HERE, "_ref", "libchpref.so")
 REF_SRC = "/root/reference/proj"
 
@@ -28,7 +29,7 @@ REF_SRC = "/root/reference/proj"
 def build(ref: bool | None = None) -> None:
     """Compile the restatement and, when the reference tree is present, the
     reference itself (oracle/_ref)."""
-    targets = [ORACLE_SO]
+    targets = [ORACLE_SO, GEN_SO]
     if ref is None:
         ref = os.path.isdir(REF_SRC)
     if ref:
@@ -38,6 +39,27 @@ def build(ref: bool | None = None) -> None:
         if os.path.exists(os.path.join(HERE, "..", "paper_1505_00914_b200", "lib", "libchp_b200.so")):
             targets.append("acceptance")
     subprocess.run(["make", "-s", "-C", HERE] + targets, check=True)
+
+
+_gen_lib = None
+
+
+def generate(config: int, seed: int, p: int, n: int, offset: int = 0, threads: int = 0) -> np.ndarray:
+    """Config 2-5 points on the host from oracle/_build/libchpgen.so (the
+    product's generator header compiled for the host), for the CPU legs that
+    must not load libchp_b200.so.  Same bytes as Context.generate."""
+    global _gen_lib
+    if _gen_lib is None:
+        if not os.path.exists(GEN_SO):
+            build(ref=False)
+        _gen_lib = ctypes.CDLL(GEN_SO)
+        _gen_lib.gen_points.restype = c_int
+        _gen_lib.gen_points.argtypes = [c_int, c_uint64, c_int64, c_uint64, c_uint64, c_void_p, c_int]
+    L = _gen_lib
+    out = np.empty((n, 2), np.int32)
+    if L.gen_points(int(config), int(seed), int(p), int(offset), int(n), _p(out), int(threads or os.cpu_count() or 1)):
+        raise ValueError(f"generate: bad config {config} / p {p}")
+    return out
 
 
 def _p(a: np.ndarray) -> c_void_p:
@@ -75,6 +97,10 @@ class Oracle:
             getattr(L, fn).restype = c_int64
             getattr(L, fn).argtypes = [c_void_p, c_int64, c_void_p]
         L.or_min_max.argtypes = [c_void_p, c_uint64, c_void_p]
+        L.or_reduce_accumulate_mt.restype = c_int
+        L.or_reduce_accumulate_mt.argtypes = [c_void_p, c_uint64, c_int64, c_int64, c_int, c_void_p, c_void_p,
+                                              c_void_p]
+        L.or_occ_from_valid.argtypes = [c_int64, c_void_p, c_void_p]
         self.L = L
 
     # -- inputs / digests
@@ -106,6 +132,10 @@ class Oracle:
         if rc != 0:
             raise ValueError("reduce: coordinate out of range")
         return {"width": int(width), "lo": lo, "hi": hi, "valid": valid, "occ": occ}
+
+    def accumulator(self, width: int, q: int | None = None) -> "Accumulator":
+        """SURVEY.md 8(c)'s chunked reduce for inputs beyond host RAM."""
+        return Accumulator(self, width, q)
 
     def L_pairs(self, arr) -> np.ndarray:
         out = np.empty((arr["width"], 2), np.int32)
@@ -187,6 +217,46 @@ class Oracle:
             return {"arr": arr, "L": L, "chain": np.empty((0, 2), np.int32), "hull": None, "s": 0}
         chain = self.build_polyline(arr)
         return {"arr": arr, "L": L, "chain": chain, "hull": self.melkman(chain), "s": len(chain)}
+
+
+class Accumulator:
+    """reduce() over a stream of chunks: each chunk is
+    reduced on host threads (src/reducer.cpp:69-79 per slice) and merged slot
+    by slot; finish() rebuilds the exact ExtremalArray by reducing the
+    survivors once more (idempotence, tests/test_reducer.cpp:113-127) and
+    checks that it reproduces the merged L."""
+
+    def __init__(self, orc: Oracle, width: int, q: int | None = None):
+        self.orc, self.width, self.q = orc, int(width), q
+        w = max(self.width, 1)
+        self.lo = np.zeros(w, np.int32)
+        self.hi = np.full(w, -1, np.int32)
+        self.valid = np.zeros(w, np.uint8)
+        self.points = 0
+
+    def add(self, xy: np.ndarray, threads: int = 0) -> None:
+        xy = np.ascontiguousarray(xy, dtype=np.int32).reshape(-1, 2)
+        rc = self.orc.L.or_reduce_accumulate_mt(_p(xy), len(xy), self.width, -1 if self.q is None else int(self.q),
+                                                int(threads or os.cpu_count() or 1), _p(self.lo), _p(self.hi),
+                                                _p(self.valid))
+        if rc != 0:
+            raise ValueError("reduce: coordinate out of range")
+        self.points += len(xy)
+
+    def finish(self):
+        w = self.width
+        occ = np.zeros((w + 63) // 64, np.uint64)
+        self.orc.L.or_occ_from_valid(w, _p(self.valid), _p(occ))
+        merged = {"width": w, "lo": self.lo.copy(), "hi": self.hi.copy(), "valid": self.valid.copy(), "occ": occ}
+        if self.orc.valid_count(merged) == 0:
+            return merged
+        survivors = self.orc.build_polyline(merged)
+        arr = self.orc.reduce(survivors, w, self.q)
+        v = arr["valid"].astype(bool)
+        assert np.array_equal(v, self.valid.astype(bool)) and np.array_equal(arr["lo"][v], self.lo[v]) \
+            and np.array_equal(arr["hi"][v], self.hi[v]) and np.array_equal(arr["occ"], occ), \
+            "re-reducing the survivors did not reproduce the merged L"
+        return arr
 
 
 class Reference:

@@ -9,6 +9,7 @@
 #include <stdlib.h>
 #include <string.h>
 #include <stdio.h>
+#include <pthread.h>
 
 typedef __int128 i128;
 
@@ -131,6 +132,94 @@ int or_reduce(const int32_t* xy, uint64_t n, int64_t width, int64_t q,
     return 0;
 }
 
+/* SURVEY.md 8(c)'s chunked procedure for inputs beyond one reduce() call:
+ * reduce() (src/reducer.cpp:69-79) per slice on `threads` host threads, each
+ * into a private (lo, hi, valid), then the slot-by-slot merge of the
+ * partials -- exact because min/max are associative and commutative, the
+ * property tests/test_reducer.cpp:113-127 pins (reducing the survivors
+ * again reproduces L).  Accumulates into the caller's arrays (initialise
+ * them once with valid = 0); the validation of src/reducer.cpp:72-75 runs on
+ * every point.  Returns 0, or -1 when the reference would throw. */
+typedef struct {
+    const int32_t* xy;
+    uint64_t n;
+    int64_t width, q;
+    int32_t *lo, *hi;
+    uint8_t* valid;
+    int rc;
+} fold_job;
+
+static void* fold_worker(void* arg) {
+    fold_job* j = (fold_job*)arg;
+    j->rc = 0;
+    for (uint64_t k = 0; k < j->n; ++k) {
+        const int64_t x = j->xy[2 * k], y = j->xy[2 * k + 1];
+        if (x < 1 || x > j->width || y < 1 || (j->q >= 0 && y > j->q)) {
+            j->rc = -1;
+            return NULL;
+        }
+    }
+    for (int64_t s = 0; s < j->width; ++s) j->valid[s] = 0;
+    or_bucket(j->xy, j->n, 0, j->lo, j->hi, j->valid, NULL);
+    return NULL;
+}
+
+int or_reduce_accumulate_mt(const int32_t* xy, uint64_t n, int64_t width, int64_t q,
+                            int threads, int32_t* lo, int32_t* hi, uint8_t* valid) {
+    if (width < 1) return -1;
+    if (threads < 1) threads = 1;
+    if (threads > 64) threads = 64;
+    if ((uint64_t)threads > n / 4096 + 1) threads = (int)(n / 4096 + 1);
+    fold_job* jobs = (fold_job*)calloc((size_t)threads, sizeof(fold_job));
+    pthread_t* tid = (pthread_t*)calloc((size_t)threads, sizeof(pthread_t));
+    int rc = 0;
+    for (int t = 0; t < threads; ++t) {
+        const uint64_t a = n * (uint64_t)t / (uint64_t)threads, b = n * (uint64_t)(t + 1) / (uint64_t)threads;
+        jobs[t].xy = xy + 2 * a;
+        jobs[t].n = b - a;
+        jobs[t].width = width;
+        jobs[t].q = q;
+        jobs[t].lo = (int32_t*)malloc((size_t)width * 4);
+        jobs[t].hi = (int32_t*)malloc((size_t)width * 4);
+        jobs[t].valid = (uint8_t*)malloc((size_t)width);
+        pthread_create(&tid[t], NULL, fold_worker, &jobs[t]);
+    }
+    for (int t = 0; t < threads; ++t) {
+        pthread_join(tid[t], NULL);
+        if (jobs[t].rc) rc = -1;
+    }
+    for (int t = 0; t < threads && rc == 0; ++t) {
+        const fold_job* j = &jobs[t];
+        for (int64_t s = 0; s < width; ++s) {
+            if (!j->valid[s]) continue;
+            if (!valid[s]) {
+                lo[s] = j->lo[s];
+                hi[s] = j->hi[s];
+                valid[s] = 1;
+            } else {
+                if (j->lo[s] < lo[s]) lo[s] = j->lo[s];
+                if (j->hi[s] > hi[s]) hi[s] = j->hi[s];
+            }
+        }
+    }
+    for (int t = 0; t < threads; ++t) {
+        free(jobs[t].lo);
+        free(jobs[t].hi);
+        free(jobs[t].valid);
+    }
+    free(jobs);
+    free(tid);
+    return rc;
+}
+
+/* The occupancy words of a merged (valid) array: Index::insert for every
+ * valid slot (include/chp/occupancy.hpp:70-74). */
+void or_occ_from_valid(int64_t width, const uint8_t* valid, uint64_t* occ) {
+    memset(occ, 0, (size_t)((width + 63) / 64) * sizeof(uint64_t));
+    for (int64_t s = 0; s < width; ++s)
+        if (valid[s]) occ_insert(occ, (uint64_t)s + 1);
+}
+
 void or_L_pairs(int64_t width, const int32_t* lo, const int32_t* hi,
                 const uint8_t* valid, int32_t* out) {
     for (int64_t s = 0; s < width; ++s) {
@@ -247,7 +336,7 @@ static void put(int32_t* xy, int64_t i, pt p) {
     xy[2 * i + 1] = (int32_t)p.y;
 }
 
-/* degenerate_hull, src/geometry.cpp:394-403 */
+/* degenerate_hull, src/geometry.cpp:29-38 */
 static int64_t degenerate(const pt* v, int64_t m, int32_t* out) {
     pt lo = v[0], hi = v[0];
     for (int64_t i = 0; i < m; ++i) {
@@ -261,7 +350,7 @@ static int64_t degenerate(const pt* v, int64_t m, int32_t* out) {
 }
 
 static int64_t canonicalize_pts(pt* v, int64_t m_in, int32_t* out) {
-    /* src/geometry.cpp:407-445 */
+    /* canonicalize_hull, src/geometry.cpp:42-80 */
     int64_t m = 0;
     for (int64_t i = 0; i < m_in; ++i)
         if (m == 0 || !pt_eq(v[m - 1], v[i])) v[m++] = v[i];
@@ -316,7 +405,7 @@ int64_t or_canonicalize(const int32_t* v_xy, int64_t m, int32_t* out) {
 }
 
 int64_t or_melkman(const int32_t* c, int64_t s, int32_t* out) {
-    /* src/hulls.cpp:396-440 */
+    /* melkman, src/hulls.cpp:137-181 */
     if (s <= 0) return -1;
     pt a = get(c, 0);
     int64_t i = 1;

@@ -35,7 +35,7 @@ uint64_t or_fnv1a64(const void* data, size_t len);
 void or_gen_uniform_box(uint64_t n, int64_t p, uint64_t seed, int32_t* xy);
 
 /* reducer::reduce, src/reducer.cpp:69-79: validation pass (:72-75) then
- * the Algorithm-1 fold `bucket` (:122-135).  lo/hi/valid have `width`
+ * the Algorithm-1 fold `bucket` (:19-32).  lo/hi/valid have `width`
  * entries, occ has ceil(width/64) words in BlockedBitset<uint64_t> layout
  * (include/chp/occupancy.hpp:46-49, :70-74).  q < 0 means "no q".
  * Returns 0, or -1 when the reference would throw std::invalid_argument. */
@@ -47,6 +47,15 @@ int or_reduce(const int32_t* xy, uint64_t n, int64_t width, int64_t q,
  * (src/reducer.cpp:19-32, translation as in :160-168). */
 void or_bucket(const int32_t* xy, uint64_t n, int64_t x_off, int32_t* lo,
                int32_t* hi, uint8_t* valid, uint64_t* occ);
+
+/* SURVEY.md 8(c) chunked procedure: reduce() per slice on host threads,
+ * merged slot by slot into the caller's (lo, hi, valid) accumulator
+ * (initialise valid to 0 once).  Returns 0 or -1 (invalid coordinate). */
+int or_reduce_accumulate_mt(const int32_t* xy, uint64_t n, int64_t width, int64_t q,
+                            int threads, int32_t* lo, int32_t* hi, uint8_t* valid);
+
+/* Occupancy words of a merged array (Index::insert per valid slot). */
+void or_occ_from_valid(int64_t width, const uint8_t* valid, uint64_t* occ);
 
 /* L in int32 (lo,hi) pairs, empty slots as the (width+1,-1) sentinel of
  * serialize(), src/reducer.cpp:121-130. */

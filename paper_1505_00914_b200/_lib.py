@@ -12,6 +12,7 @@ from ctypes import POINTER, c_char_p, c_int, c_int32, c_int64, c_uint32, c_uint6
 from ._build import LIB
 
 CHP_OK, CHP_EINVAL, CHP_EDEVICE = 0, 1, 2
+COMBINE_NCCL, COMBINE_PEER = 0, 1
 REDUCE_ACCUMULATE = 1
 REDUCE_NO_VALIDATE = 2
 REDUCE_FORCE_GLOBAL = 4
@@ -72,6 +73,18 @@ def load() -> ctypes.CDLL:
         "chp_pipeline_host64": (c_int, [vp, vp, c_uint64, c_int64, c_int64, vp, vp, vp, vp, vp, vp]),
         "chp_precondition_run64": (c_int, [vp, vp, c_uint64, c_int, c_int, vp, vp, vp, vp]),
         "chp_bounds_host64": (c_int, [vp, vp, c_uint64, vp]),
+        "chp_reduce_host": (c_int, [vp, vp, c_uint64, c_int64, c_int64, vp]),
+        "chp_reduce_host64": (c_int, [vp, vp, c_uint64, c_int64, c_int64, vp]),
+        "chp_finish_host": (c_int, [vp, vp, c_int64, vp, vp, vp, vp, vp, vp]),
+        "chp_group_create": (c_int, [vp, c_int, c_int, POINTER(c_void_p)]),
+        "chp_group_destroy": (None, [vp]),
+        "chp_group_ctx": (vp, [vp, c_int]),
+        "chp_group_size": (c_int, [vp]),
+        "chp_group_last_error": (c_char_p, [vp]),
+        "chp_group_last_h2d_bytes": (c_uint64, [vp]),
+        "chp_reduce_sharded": (c_int, [vp, vp, vp, c_int64, c_int64, vp]),
+        "chp_pipeline_host_sharded": (c_int, [vp, vp, c_uint64, c_int64, c_int64, vp, vp, vp, vp, vp, vp]),
+        "chp_pipeline_host64_sharded": (c_int, [vp, vp, c_uint64, c_int64, c_int64, vp, vp, vp, vp, vp, vp]),
         "chp_generate": (c_int, [vp, c_int, c_uint64, c_int64, c_uint64, c_uint64, vp]),
         "chp_generate_host": (c_int, [c_int, c_uint64, c_int64, c_uint64, c_uint64, vp, c_int]),
     }
@@ -89,5 +102,8 @@ ABI_SYMBOLS = (
     "chp_ctx_sync", "chp_launch_count", "chp_last_variant", "chp_last_h2d_bytes", "chp_dl_len", "chp_reduce", "chp_dl_init",
     "chp_check", "chp_dl_from_pairs", "chp_polyline_host", "chp_compact", "chp_ns_chain", "chp_hull", "chp_bounds", "chp_translate", "chp_translate_host",
     "chp_pipeline_host", "chp_precondition_host", "chp_precondition_run", "chp_last_outputs", "chp_pipeline_host64", "chp_precondition_run64",
-    "chp_bounds_host64", "chp_generate", "chp_generate_host",
+    "chp_bounds_host64", "chp_reduce_host", "chp_reduce_host64", "chp_finish_host", "chp_group_create",
+    "chp_group_destroy", "chp_group_ctx", "chp_group_size", "chp_group_last_error", "chp_group_last_h2d_bytes",
+    "chp_reduce_sharded", "chp_pipeline_host_sharded", "chp_pipeline_host64_sharded", "chp_generate",
+    "chp_generate_host",
 )

@@ -112,7 +112,8 @@ class HostPool {
 HostPool* pool_of(chp_ctx* ctx) {
     if (!ctx->pool) {
         const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-        ctx->pool = new HostPool((int)std::min(hw, 32u) - 1);
+        const int parts = ctx->pool_parts > 0 ? ctx->pool_parts : (int)std::min(hw, 32u);
+        ctx->pool = new HostPool(std::max(parts, 1) - 1);
     }
     return static_cast<HostPool*>(ctx->pool);
 }
@@ -567,10 +568,10 @@ bool pack_window(chp_ctx* ctx, const HostPts& in, uint64_t n, int64_t* wx, int64
 // whose slots and y offsets fit 16 bits travel packed (half the PCIe bytes)
 // unless CHP_PIPELINE_NO_PACK is set in flags or the environment.
 int stream_reduce(chp_ctx* ctx, const HostPts& in, uint64_t n, int64_t width, int64_t ybase, int64_t ycount,
-                  int64_t x_off, uint32_t flags) {
+                  int64_t x_off, uint32_t flags, int32_t* d_L = nullptr) {
+    if (!d_L) d_L = (int32_t*)ctx->dl.p;
     auto launch = [&](const int32_t* d, uint64_t m) {
-        return chp_reduce_yr(ctx, d, m, width, ybase, ycount, x_off, (int32_t*)ctx->dl.p,
-                             flags | CHP_REDUCE_ACCUMULATE);
+        return chp_reduce_yr(ctx, d, m, width, ybase, ycount, x_off, d_L, flags | CHP_REDUCE_ACCUMULATE);
     };
     // ycount < 0 (no upper bound, the reference's default q = nullopt):
     // pack speculatively against a 2^16 window; chunks with a larger y go
@@ -602,17 +603,18 @@ int stream_reduce(chp_ctx* ctx, const HostPts& in, uint64_t n, int64_t width, in
     }
     if (bad) {  // same outcome as the unpacked path: the error word of DL
         int32_t minus1 = -1;
-        CHP_CUDA(ctx, cudaMemcpyAsync((int32_t*)ctx->dl.p + 2 * width, &minus1, 4, cudaMemcpyHostToDevice,
+        CHP_CUDA(ctx, cudaMemcpyAsync(d_L + 2 * width, &minus1, 4, cudaMemcpyHostToDevice,
                                       ctx->stream));
         CHP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     }
     return CHP_OK;
 }
 
-// Compaction (+ hull) of ctx->dl into the context's device buffers; cnt
-// receives the K3/K4 counts {s, v, err, s-v, h}.
+// Compaction (+ hull) of d_L (default ctx->dl) into the context's device
+// buffers; cnt receives the K3/K4 counts {s, v, err, s-v, h}.
 int finish_device(chp_ctx* ctx, int64_t width, int64_t major_off, int64_t minor_off, bool want_chain,
-                  bool want_lpairs, bool want_occ, bool want_hull, int64_t cnt[8]) {
+                  bool want_lpairs, bool want_occ, bool want_hull, int64_t cnt[8], const int32_t* d_L = nullptr) {
+    if (!d_L) d_L = (const int32_t*)ctx->dl.p;
     int rc;
     const size_t W = (size_t)width;
     if ((rc = chp_ensure(ctx, ctx->counts, 16 * sizeof(int64_t)))) return rc;
@@ -625,7 +627,7 @@ int finish_device(chp_ctx* ctx, int64_t width, int64_t major_off, int64_t minor_
         if ((rc = chp_ensure(ctx, ctx->hull, (2 * W + 4) * 8))) return rc;
     }
     int64_t* d_counts = (int64_t*)ctx->counts.p;
-    if ((rc = chp_compact(ctx, (const int32_t*)ctx->dl.p, width, major_off, minor_off, 0,
+    if ((rc = chp_compact(ctx, d_L, width, major_off, minor_off, 0,
                           want_chain ? (int32_t*)ctx->chain.p : nullptr, want_occ ? (uint64_t*)ctx->occ.p : nullptr,
                           want_lpairs ? (int32_t*)ctx->lpairs.p : nullptr,
                           want_hull ? (int32_t*)ctx->lower.p : nullptr,
@@ -658,14 +660,15 @@ int copy_out(chp_ctx* ctx, int64_t width, int64_t s, int64_t h, int32_t* h_Lpair
     return CHP_OK;
 }
 
-// Compaction (+ hull) of ctx->dl, then the requested outputs to the host.
+// Compaction (+ hull) of d_L (default ctx->dl), then the requested outputs
+// to the host.
 int finish_host(chp_ctx* ctx, int64_t width, int64_t major_off, int64_t minor_off, int32_t* h_Lpairs,
                 uint64_t* h_occ, int32_t* h_chain, int64_t* h_s, int32_t* h_hull, int64_t* h_h,
-                bool chain_required) {
+                bool chain_required, const int32_t* d_L = nullptr) {
     int64_t cnt[8];
     const bool want_hull = h_hull || h_h;
     int rc = finish_device(ctx, width, major_off, minor_off, h_chain || h_s, h_Lpairs != nullptr, h_occ != nullptr,
-                           want_hull, cnt);
+                           want_hull, cnt, d_L);
     if (rc) return rc;
     if (cnt[2] != 0) return chp_einval(ctx, "reduce: coordinate out of range");
     const int64_t s = cnt[0];
@@ -795,6 +798,41 @@ int chp_pipeline_host64(chp_ctx* ctx, const int64_t* h_xy, uint64_t n, int64_t w
     HostPts in;
     in.p64 = h_xy;
     return pipeline_core(ctx, in, n, width, q, h_Lpairs, h_occ, h_chain, h_s, h_hull, h_h);
+}
+
+static int reduce_host_core(chp_ctx* ctx, const HostPts& in, uint64_t n, int64_t width, int64_t q, int32_t* d_L) {
+    if (!ctx || !d_L) return CHP_EINVAL;
+    ctx->h2d_bytes = 0;
+    ctx->last_valid = false;
+    if (width < 1) return chp_einval(ctx, "reduce: width must be >= 1");
+    if (width > (1ll << 29)) return chp_einval(ctx, "reduce: width exceeds the device limit 2^29");
+    CHP_CUDA(ctx, cudaSetDevice(ctx->device));
+    int rc;
+    if ((rc = chp_dl_init(ctx, d_L, width))) return rc;
+    if ((rc = stream_reduce(ctx, in, n, width, 1, q, 0, 0, d_L))) return rc;
+    CHP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return CHP_OK;
+}
+
+int chp_reduce_host(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t width, int64_t q, int32_t* d_L) {
+    HostPts in;
+    in.p32 = h_xy;
+    return reduce_host_core(ctx, in, n, width, q, d_L);
+}
+
+int chp_reduce_host64(chp_ctx* ctx, const int64_t* h_xy, uint64_t n, int64_t width, int64_t q, int32_t* d_L) {
+    HostPts in;
+    in.p64 = h_xy;
+    return reduce_host_core(ctx, in, n, width, q, d_L);
+}
+
+int chp_finish_host(chp_ctx* ctx, const int32_t* d_L, int64_t width, int32_t* h_Lpairs, uint64_t* h_occ,
+                    int32_t* h_chain, int64_t* h_s, int32_t* h_hull, int64_t* h_h) {
+    if (!ctx || !d_L) return CHP_EINVAL;
+    if (width < 1 || width > (1ll << 29)) return chp_einval(ctx, "compact: width out of range");
+    CHP_CUDA(ctx, cudaSetDevice(ctx->device));
+    return finish_host(ctx, width, 0, 0, h_Lpairs, h_occ, h_chain, h_s, h_hull, h_h,
+                       h_chain != nullptr || h_hull != nullptr, d_L);
 }
 
 int chp_translate_host(chp_ctx* ctx, const int32_t* h_in, uint64_t n, int32_t dx, int32_t dy, int32_t* h_out) {

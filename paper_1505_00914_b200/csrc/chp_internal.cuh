@@ -55,6 +55,7 @@ struct chp_ctx {
     size_t pack_bytes = 0;
     DevBuf unpack_dev[2];
     void* pool = nullptr;
+    int pool_parts = 0;      // host threads of the pool (0: all cores, <= 32); shard groups split the cores
     uint64_t h2d_bytes = 0;  // of the current / last host pipeline call
     // Hybrid packed pipeline: int32 chunks DMA'd straight from a pinned input
     // while the host packs (abi.cu), and the measured host pack rate.

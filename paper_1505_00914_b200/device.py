@@ -243,6 +243,50 @@ class Context:
                                              None if chain_ptr is None else c_void_p(chain_ptr),
                                              _np_ptr(s_out), None, None))
 
+    def reduce_host_ptr(self, xy_ptr: int, n: int, width: int, q: int | None, DL: torch.Tensor) -> None:
+        """chp_reduce_host: HOST points (raw pointer; pinned is fastest) into a
+        device DL, initialised here; the error word stays in DL (combine
+        partials first, then finish_host raises)."""
+        self._stream()
+        self._check(self.L.chp_reduce_host(self.h, c_void_p(xy_ptr), int(n), int(width), -1 if q is None else int(q),
+                                           _ptr(DL)))
+
+    def reduce_host(self, xy: np.ndarray, width: int, q: int | None = None,
+                    out: torch.Tensor | None = None) -> torch.Tensor:
+        xy = np.ascontiguousarray(xy, dtype=np.int32)
+        DL = out if out is not None else self.empty_dl(width)
+        self.reduce_host_ptr(xy.ctypes.data, xy.size // 2, width, q, DL)
+        return DL
+
+    def finish_host_ptr(self, DL: torch.Tensor, width: int, chain_ptr: int | None, s_out: np.ndarray) -> None:
+        """chp_finish_host: K3 of a device DL, chain to a host pointer."""
+        self._stream()
+        self._check(self.L.chp_finish_host(self.h, _ptr(DL), int(width), None, None,
+                                           None if chain_ptr is None else c_void_p(chain_ptr), _np_ptr(s_out),
+                                           None, None))
+
+    def finish_host(self, DL: torch.Tensor, width: int, L: bool = False, chain: bool = True,
+                    hull: bool = False) -> dict:
+        """K3 (+K4) of a device DL, outputs in host memory (ValueError when
+        DL's error word is set, as pipeline_host)."""
+        self._stream()
+        w = int(width)
+        Lp = np.empty((w, 2), np.int32) if L else None
+        ch = np.empty((2 * w, 2), np.int32) if chain else None
+        hl = np.empty((2 * w + 2, 2), np.int32) if hull else None
+        s = np.zeros(1, np.int64)
+        h = np.zeros(1, np.int64)
+        self._check(self.L.chp_finish_host(self.h, _ptr(DL), w, _np_ptr(Lp), None, _np_ptr(ch), _np_ptr(s),
+                                           _np_ptr(hl), _np_ptr(h) if hull else None))
+        out = {"s": int(s[0])}
+        if L:
+            out["L"] = Lp
+        if chain:
+            out["chain"] = ch[: int(s[0])]
+        if hull:
+            out["hull"] = hl[: int(h[0])]
+        return out
+
     def polyline_host(self, lpairs: np.ndarray, width: int, major_off: int = 0, minor_off: int = 0,
                       swapped: bool = False) -> np.ndarray:
         lp = np.ascontiguousarray(lpairs, dtype=np.int32)
@@ -277,6 +321,106 @@ class Context:
                "L": Lp, "chain": ch, "s": s}
         if hull:
             out["hull"] = hl[:h]
+        return out
+
+
+class Group:
+    """A shard group (include/chp_b200.h chp_group_*): reduce over G devices
+    of this box in one process, partial Ls merged by ONE element-wise MIN --
+    ncclAllReduce (combine="nccl", distinct devices) or one peer-memory
+    kernel on device 0 (combine="peer"; devices may repeat)."""
+
+    def __init__(self, devices, combine: str = "nccl"):
+        self.L = _lib.load()
+        devs = (ctypes.c_int * len(devices))(*[int(d) for d in devices])
+        mode = {"nccl": _lib.COMBINE_NCCL, "peer": _lib.COMBINE_PEER}[combine]
+        h = c_void_p()
+        rc = self.L.chp_group_create(devs, len(devices), mode, byref(h))
+        if rc != CHP_OK:
+            raise (ValueError if rc == CHP_EINVAL else ChpError)(
+                f"chp_group_create({list(devices)}, {combine}) failed (rc={rc})")
+        self.h = h
+        self.devices = [int(d) for d in devices]
+        self.combine = combine
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.chp_group_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def size(self) -> int:
+        return int(self.L.chp_group_size(self.h))
+
+    @property
+    def last_h2d_bytes(self) -> int:
+        return int(self.L.chp_group_last_h2d_bytes(self.h))
+
+    @property
+    def launches(self) -> int:
+        return sum(int(self.L.chp_launch_count(self.L.chp_group_ctx(self.h, k))) for k in range(self.size))
+
+    def _check(self, rc: int):
+        if rc == CHP_OK:
+            return
+        msg = (self.L.chp_group_last_error(self.h) or b"").decode()
+        if rc == CHP_EINVAL:
+            raise ValueError(msg)
+        raise ChpError(msg)
+
+    def reduce_sharded(self, shards, width: int, q: int | None = None, outs=None):
+        """Device-resident shards (one (n_k, 2) int32 CUDA tensor per group
+        device).  Returns the per-shard DLs; DL 0 holds the merged L (NCCL:
+        every DL does).  Runs on each shard context's own stream."""
+        G = self.size
+        if len(shards) != G:
+            raise ValueError(f"{len(shards)} shards for a group of {G}")
+        outs = outs if outs is not None else [
+            torch.empty(int(self.L.chp_dl_len(int(width))), dtype=torch.int32, device=t.device) for t in shards]
+        for t in shards:
+            Context._xy(t)
+        # the shard contexts run on their own streams: order them after the
+        # producers of the inputs / outputs on torch's current streams
+        for k, t in enumerate(shards):
+            torch.cuda.current_stream(t.device).synchronize()
+        xs = (c_void_p * G)(*[t.data_ptr() for t in shards])
+        ns = (ctypes.c_uint64 * G)(*[t.numel() // 2 for t in shards])
+        ds = (c_void_p * G)(*[d.data_ptr() for d in outs])
+        self._check(self.L.chp_reduce_sharded(self.h, xs, ns, int(width), -1 if q is None else int(q), ds))
+        for k in range(G):
+            self.L.chp_ctx_sync(self.L.chp_group_ctx(self.h, k))
+        return outs
+
+    def pipeline_host(self, xy: np.ndarray, width: int, q: int | None = None, L: bool = False, occ: bool = False,
+                      chain: bool = True, hull: bool = False) -> dict:
+        """chp_pipeline_host_sharded: the host input split over the group."""
+        xy = np.ascontiguousarray(xy, dtype=np.int32)
+        w = int(width)
+        n = xy.size // 2
+        Lp = np.empty((max(w, 1), 2), np.int32) if L else None
+        oc = np.empty(((max(w, 1) + 63) // 64,), np.uint64) if occ else None
+        ch = np.empty((2 * max(w, 1), 2), np.int32) if chain else None
+        hl = np.empty((2 * max(w, 1) + 2, 2), np.int32) if hull else None
+        s = np.zeros(1, np.int64)
+        h = np.zeros(1, np.int64)
+        self._check(self.L.chp_pipeline_host_sharded(self.h, _np_ptr(xy), n, w, -1 if q is None else int(q),
+                                                     _np_ptr(Lp), _np_ptr(oc), _np_ptr(ch), _np_ptr(s), _np_ptr(hl),
+                                                     _np_ptr(h) if hull else None))
+        out = {"s": int(s[0])}
+        if L:
+            out["L"] = Lp[:w]
+        if occ:
+            out["occ"] = oc
+        if chain:
+            out["chain"] = ch[: int(s[0])]
+        if hull:
+            out["hull"] = hl[: int(h[0])]
         return out
 
 

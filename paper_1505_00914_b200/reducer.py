@@ -107,11 +107,11 @@ class ExtremalArray:
         return self._chain
 
     def valid_count(self) -> int:
-        """reducer.cpp:42-49"""
+        """src/reducer.cpp:42-49"""
         return int(len(self._device_chain()))
 
     def valid_points(self) -> np.ndarray:
-        """reducer.cpp:154-163 (slot order, lo before hi)."""
+        """src/reducer.cpp:51-60 (slot order, lo before hi)."""
         return self._device_chain().copy()
 
 

@@ -125,3 +125,38 @@ def test_oracle_matches_reference_precondition(orc, ref):
         assert r["major_offset"] == o["bbox"][0] - 1 and r["minor_offset"] == 0
         assert np.array_equal(r["chain"], o["chain"])
         assert np.array_equal(r["hull"], o["hull"])
+
+
+def test_host_generator_lib_matches_product():
+    """oracle/_build/libchpgen.so (what the CPU legs load instead of the
+    product library) emits the product generator's bytes."""
+    import oracle
+    from paper_1505_00914_b200.device import generate_host
+
+    for config, p in ((2, 65536), (3, 16384), (4, 1 << 20), (5, 256)):
+        a = oracle.generate(config, config, p, 200_003, offset=987_654_321)
+        b = generate_host(config, config, p, 200_003, offset=987_654_321)
+        assert np.array_equal(a, b), config
+
+
+def test_chunked_accumulator_matches_one_shot(orc):
+    """SURVEY.md 8(c)'s chunked reduce (the full-size parity tests' oracle)
+    equals one reduce() over the whole input."""
+    import oracle
+
+    for config, p in ((4, 1 << 20), (5, 256), (2, 4096)):
+        xy = oracle.generate(config, config, p, 3_000_000)
+        one = orc.reduce(xy, p, p)
+        acc = orc.accumulator(p, p)
+        for a in range(0, len(xy), 700_001):
+            acc.add(xy[a:a + 700_001], threads=7)
+        got = acc.finish()
+        for k in ("lo", "hi", "valid", "occ"):
+            v = one["valid"].astype(bool)
+            if k in ("lo", "hi"):
+                assert np.array_equal(got[k][v], one[k][v]), k
+            else:
+                assert np.array_equal(got[k], one[k]), k
+    acc = orc.accumulator(10, 10)
+    with pytest.raises(ValueError):
+        acc.add(np.array([[1, 1], [11, 1]], np.int32))

@@ -88,6 +88,9 @@ DOWNSCALED = [  # (config, p, n)
     (4, 1 << 20, 3_000_000),
     (4, 8192, 1_000_000),
     (5, 256, 3_000_000),
+    # >= 4 Mi points: the q-known group filter's phased mode (snapshot
+    # rebuilds between phases of doubling length, csrc/reduce.cu plan_for)
+    (4, 1 << 20, 10_000_000),
 ]
 
 
@@ -225,6 +228,75 @@ def test_full_size_config2_vs_oracle(ctx, orc):
     assert np.array_equal(comp["chain"][: int(c[0])].cpu().numpy(), chain)
     h = int(hull["h"].item())
     assert np.array_equal(hull["hull"][:h].cpu().numpy(), orc.melkman(chain))
+
+
+def _host_mem_available() -> int:
+    with open("/proc/meminfo") as f:
+        for line in f:
+            if line.startswith("MemAvailable:"):
+                return int(line.split()[1]) * 1024
+    return 0
+
+
+FULL_VARIANTS = ("auto", "global", "filter", "sampled", "smem16")
+
+
+@pytest.mark.parametrize("config", [3, 4, 5])
+def test_full_size_vs_oracle(ctx, orc, config):
+    """BASELINE.json configs 3-5 at full size (1e9 / 1e9 / 4e9 points)
+    against the oracle, bit for bit: L (serialize form), occupancy words,
+    s, the Lemma-1 chain, the north_star chain and the hull, for the auto
+    variant and every forced K1 variant.  The oracle reads the device's own
+    input bytes back in 1 GB chunks and reduces them with SURVEY.md 8(c)'s
+    chunked procedure (reduce per slice on host threads, slot-by-slot merge,
+    then the survivors reduced once more), so nothing of 8-32 GB has to sit
+    in host memory at once."""
+    import bench
+
+    n, p, seed, _ = bench.CONFIGS[config]
+    need_host = (1 << 30) + 64 * 9 * p + (2 << 30)
+    if _host_mem_available() < need_host:
+        pytest.skip(f"needs ~{need_host / 2**30:.1f} GiB of available host RAM (1 GiB pinned chunk + oracle tables)")
+    free = torch.cuda.mem_get_info()[0]
+    if n * 8 + (1 << 30) > free:
+        pytest.skip(f"needs {(n * 8 + (1 << 30)) / 2**30:.1f} GiB of free device memory")
+    d = ctx.generate(config, seed, p, n)
+    got = {}
+    for name in FULL_VARIANTS:
+        DL = ctx.reduce(d, p, q=p, flags=VARIANTS[name])
+        comp = ctx.compact(DL, p, chain=True, occ=True, lpairs=True, lower=True, upper=True, upperd=True)
+        hull = ctx.hull(comp, p)
+        ns = ctx.ns_chain(comp, p)
+        torch.cuda.synchronize()
+        c = comp["counts"].cpu().numpy()
+        s, h = int(c[0]), int(hull["h"].item())
+        got[name] = {"variant": ctx.variant, "err": int(c[2]), "s": s, "L": comp["lpairs"].cpu().numpy(),
+                     "occ": comp["occ"].cpu().numpy().view(np.uint64), "chain": comp["chain"][:s].cpu().numpy(),
+                     "ns": ns[:s].cpu().numpy(), "hull": hull["hull"][:h].cpu().numpy()}
+        del DL, comp, hull, ns
+    acc = orc.accumulator(p, p)
+    chunk = 1 << 27  # points (1 GiB)
+    host = torch.empty((chunk, 2), dtype=torch.int32, pin_memory=True)
+    for a in range(0, n, chunk):
+        m = min(chunk, n - a)
+        host[:m].copy_(d[a:a + m])
+        acc.add(host[:m].numpy())
+    assert acc.points == n
+    del host, d
+    arr = acc.finish()
+    L = orc.L_pairs(arr)
+    chain = orc.build_polyline(arr)
+    ns = orc.ns_chain(arr)
+    hull = orc.melkman(chain)
+    for name, g in got.items():
+        tag = f"config {config}, variant {name} ({g['variant']})"
+        assert g["err"] == 0, tag
+        assert np.array_equal(g["L"], L), "L mismatch: " + tag
+        assert np.array_equal(g["occ"], arr["occ"]), "occupancy mismatch: " + tag
+        assert g["s"] == len(chain), tag
+        assert np.array_equal(g["chain"], chain), "Lemma-1 chain mismatch: " + tag
+        assert np.array_equal(g["ns"], ns), "north_star chain mismatch: " + tag
+        assert np.array_equal(g["hull"], hull), "hull mismatch: " + tag
 
 
 @pytest.mark.parametrize("config", [3, 4, 5])
