@@ -60,7 +60,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", type=int, default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
-    ap.add_argument("--n", type=int, default=0, help="override the config's total n (tests, smoke runs)")
+    ap.add_argument("--total-points", type=int, default=0,
+                    help="override the config's total n (tests, smoke runs)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--flags", type=int, default=0, help="chp_reduce flags (variant forcing, experiments)")
     ap.add_argument("--q-unset", action="store_true",
@@ -206,7 +207,7 @@ def run_reference(args):
     rank, world, _ = env_rank()
     if rank != 0:
         return 0
-    n_total = args.n or CONFIGS[args.config][0]
+    n_total = args.total_points or CONFIGS[args.config][0]
     n_sample = min(n_total, REF_SAMPLE)
     threads = os.cpu_count() or 1
     step, kind, threads = cpu_time_sample(args.config, n_sample, threads=threads, reps=1)
@@ -357,7 +358,7 @@ class Arm:
         k1_avg = sum(k1_ms) / len(k1_ms)
         achieved = 8.0 * n / (k1_avg * 1e-3) / 1e9
         peak, peak_src = measured_peak()
-        traffic, traffic_src = committed_traffic(cfg) if self.world == 1 and not args.n else (None, None)
+        traffic, traffic_src = committed_traffic(cfg) if self.world == 1 and not args.total_points else (None, None)
         out = {
             "value": n_total / (ms_per_step * 1e-3) / 1e9, "ms_per_step": ms_per_step,
             "ms_per_step_best": min(step_ms), "ms_per_step_median": statistics.median(step_ms),
@@ -494,13 +495,13 @@ def main():
     if args.impl == "reference":
         return run_reference(args)
     arm = Arm(args)
-    n_total = args.n or CONFIGS[args.config][0]
+    n_total = args.total_points or CONFIGS[args.config][0]
     head = arm.measure(args.config, n_total, e2e=not args.no_e2e)
     pre = None
     if arm.world == 1 and not args.no_e2e:
         pre = arm.precondition_e2e(args.config, n_total)
     per_config = {}
-    if not args.no_per_config and args.config == DEFAULT_CONFIG and not args.n:
+    if not args.no_per_config and args.config == DEFAULT_CONFIG and not args.total_points:
         for c in sorted(CONFIGS):
             if c == args.config:
                 continue

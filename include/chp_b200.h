@@ -58,7 +58,10 @@ void chp_ctx_destroy(chp_ctx* ctx);
 const char* chp_last_error(const chp_ctx* ctx);
 /* Run on a caller-owned cudaStream_t (e.g. torch's current stream); NULL is
  * the legacy default stream.  chp_ctx_use_own_stream() switches back to the
- * context's own non-blocking stream (the initial state). */
+ * context's own non-blocking stream (the initial state).  A switch orders
+ * the new stream after all work the context issued on the old one (the
+ * context's scratch is shared by its calls), so one context's calls never
+ * overlap, whatever streams they are issued on. */
 int chp_ctx_set_stream(chp_ctx* ctx, void* cuda_stream);
 int chp_ctx_use_own_stream(chp_ctx* ctx);
 void* chp_ctx_stream(const chp_ctx* ctx);

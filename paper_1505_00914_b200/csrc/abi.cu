@@ -690,6 +690,7 @@ int chp_ctx_create(int device, chp_ctx** out) {
     cudaError_t e = cudaSetDevice(device);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_switch, cudaEventDisableTiming);
     for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
         e = cudaEventCreateWithFlags(&ctx->ev_copied[b], cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_consumed[b], cudaEventDisableTiming);
@@ -734,6 +735,7 @@ void chp_ctx_destroy(chp_ctx* ctx) {
         if (ctx->ev_copied[b]) cudaEventDestroy(ctx->ev_copied[b]);
         if (ctx->ev_consumed[b]) cudaEventDestroy(ctx->ev_consumed[b]);
     }
+    if (ctx->ev_switch) cudaEventDestroy(ctx->ev_switch);
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
@@ -741,16 +743,30 @@ void chp_ctx_destroy(chp_ctx* ctx) {
 
 const char* chp_last_error(const chp_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
+// The context's scratch (filter / sample tables, grid barrier, look-back
+// status words, hull buffers, pipeline staging) is shared by every call, so
+// a stream switch orders the new stream after everything the context has
+// issued on the old one (and on its copy stream): a context's work never
+// overlaps itself, whichever streams a caller hands it.
+static int switch_stream(chp_ctx* ctx, cudaStream_t s) {
+    if (s == ctx->stream) return CHP_OK;
+    CHP_CUDA(ctx, cudaSetDevice(ctx->device));
+    CHP_CUDA(ctx, cudaEventRecord(ctx->ev_switch, ctx->stream));
+    CHP_CUDA(ctx, cudaStreamWaitEvent(s, ctx->ev_switch, 0));
+    CHP_CUDA(ctx, cudaEventRecord(ctx->ev_switch, ctx->copy_stream));
+    CHP_CUDA(ctx, cudaStreamWaitEvent(s, ctx->ev_switch, 0));
+    ctx->stream = s;
+    return CHP_OK;
+}
+
 int chp_ctx_set_stream(chp_ctx* ctx, void* stream) {
     if (!ctx) return CHP_EINVAL;
-    ctx->stream = (cudaStream_t)stream;
-    return CHP_OK;
+    return switch_stream(ctx, (cudaStream_t)stream);
 }
 
 int chp_ctx_use_own_stream(chp_ctx* ctx) {
     if (!ctx) return CHP_EINVAL;
-    ctx->stream = ctx->own_stream;
-    return CHP_OK;
+    return switch_stream(ctx, ctx->own_stream);
 }
 
 void* chp_ctx_stream(const chp_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }

@@ -47,6 +47,7 @@ struct chp_ctx {
     DevBuf stage_dev[2]; // host pipeline: device input chunks
     void* stage_host[2] = {nullptr, nullptr};  // pinned staging for pageable inputs
     size_t stage_bytes = 0;
+    cudaEvent_t ev_switch = nullptr;  // chp_ctx_set_stream: the old stream's work before the new one's
     cudaEvent_t ev_copied[2] = {nullptr, nullptr};
     cudaEvent_t ev_consumed[2] = {nullptr, nullptr};
     // Packed host pipeline: pinned 4-byte/point staging, unpacked device
@@ -133,18 +134,23 @@ __device__ __forceinline__ int4 ld_stream(const int4* p) {
                  : "l"(p));
     return r;
 }
-// Grid-wide barrier of a cooperative launch (every CTA co-resident).
+// Grid-wide barrier of a cooperative launch (every CTA co-resident).  Each
+// launch starts with count == 0 and leaves it 0: after its LAST barrier
+// every CTA calls grid_barrier_done(), and the final one to do so resets
+// the words (no CTA polls the counter any more by then).  A launch that is
+// refused never touches the words; two cooperative kernels of one context
+// never overlap (chp_ctx_set_stream orders the context's streams).  So no
+// launch depends on another's grid size or barrier count.
 struct GridBar {
-    unsigned long long count;  // arrivals since the context was created (see grid_barrier)
+    unsigned long long count;  // arrivals in the current launch
+    unsigned long long exits;  // CTAs past their last barrier
 };
 
 __device__ __forceinline__ void grid_barrier(GridBar* b) {
-    // One atomic per CTA and no reset: arrival k of barrier round r sees
-    // old = r * G + k, and the round is complete once the 64-bit counter
-    // reaches (r + 1) * G.  Every cooperative launch on a context uses the
-    // same grid size G (one CTA per SM).  The last arrival's add releases
-    // everyone directly (the reset-and-flip form needed two more serialised
-    // L2 round trips, ~2 us at 148 CTAs).
+    // One atomic per CTA: arrival k of barrier round r sees old = r * G + k,
+    // and the round is complete once the counter reaches (r + 1) * G.  The
+    // last arrival's add releases everyone directly (the reset-and-flip form
+    // needed two more serialised L2 round trips, ~2 us at 148 CTAs).
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
@@ -161,6 +167,18 @@ __device__ __forceinline__ void grid_barrier(GridBar* b) {
         __threadfence();
     }
     __syncthreads();
+}
+
+// After a CTA's last grid_barrier of the launch (thread 0 has observed the
+// release, so it no longer reads the counter).
+__device__ __forceinline__ void grid_barrier_done(GridBar* b) {
+    if (threadIdx.x == 0) {
+        const unsigned long long old = atomicAdd(&b->exits, 1ull);
+        if (old == gridDim.x - 1ull) {
+            atomicExch(&b->count, 0ull);
+            atomicExch(&b->exits, 0ull);
+        }
+    }
 }
 
 // L2-coherent load of a slot pair that other CTAs update atomically.

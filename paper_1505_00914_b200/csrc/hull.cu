@@ -303,6 +303,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1)
         nregions = npairs;
         region_cap *= 2;
     }
+    grid_barrier_done(bar);
     if (blockIdx.x == 0) final_block(bin, cin, nchunks, cap, counts, swapped, tmp, hull, h_out);
 }
 
@@ -355,7 +356,11 @@ extern "C" int chp_hull(chp_ctx* ctx, const int32_t* d_lower, const int32_t* d_u
                             (void*)&bufs[0], (void*)&bufs[1], (void*)&cnts[0], (void*)&cnts[1], (void*)&sw,
                             (void*)&tmp,     (void*)&hp,      (void*)&hh,     (void*)&bar};
             // (Refused when the grid cannot be co-resident: the launches below.)
-            if (cudaLaunchCooperativeKernel((const void*)k_hull_coop, dim3(ctx->sm_count), dim3(kCoopThreads), args,
+            // CHP_TEST_COOP_REFUSE (tests): an oversized grid, which the
+            // runtime refuses without running anything.
+            static const bool refuse = getenv("CHP_TEST_COOP_REFUSE") != nullptr;
+            if (cudaLaunchCooperativeKernel((const void*)k_hull_coop, dim3(ctx->sm_count * (refuse ? 64 : 1)),
+                                            dim3(kCoopThreads), args,
                                             kLeafSmem, ctx->stream) == cudaSuccess) {
                 CHP_LAUNCHED(ctx);
                 return CHP_OK;

@@ -1126,6 +1126,7 @@ __global__ void __launch_bounds__(kThreads) k_sampled_fused(const int32_t* __res
     sample_dump(smem4, scratch, wpad);
     phase_mark(3);
     grid_barrier(bar);
+    if (merge_only) grid_barrier_done(bar);
     phase_mark(4);
     // ---- B: merge; this CTA owns chunks [c0, c1), 64 chunks x 16 slices
     {
@@ -1162,6 +1163,7 @@ __global__ void __launch_bounds__(kThreads) k_sampled_fused(const int32_t* __res
     phase_mark(5);
     if (merge_only) return;  // the main pass is a separate (dependent) launch
     grid_barrier(bar);
+    grid_barrier_done(bar);
     // ---- C: every CTA loads the merged table
     {
         const uint4* F4 = reinterpret_cast<const uint4*>(F);
@@ -1593,7 +1595,8 @@ int chp_reduce_yr(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t width, 
                     // (A cooperative launch can be refused when the GPU is
                     // shared and the grid cannot be co-resident: then the
                     // split form below runs instead.)
-                    const cudaError_t ce = cudaLaunchCooperativeKernel(fused, dim3(sblocks),
+                    static const bool refuse = getenv("CHP_TEST_COOP_REFUSE") != nullptr;  // tests
+                    const cudaError_t ce = cudaLaunchCooperativeKernel(fused, dim3(sblocks * (refuse ? 64 : 1)),
                                                                        dim3(kThreads), args, smem, ctx->stream);
                     if (ce != cudaSuccess) {
                         cudaGetLastError();

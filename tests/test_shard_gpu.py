@@ -127,7 +127,7 @@ def test_bench_two_ranks_gloo_verified(config, n):
     env = {**os.environ, "CHP_DIST_BACKEND": "gloo"}
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr=127.0.0.1", f"--master-port={_free_port()}", "bench.py", "--gpus", "2",
-           "--config", str(config), "--n", str(n), "--steps", "3", "--warmup", "3", "--e2e-steps", "2",
+           "--config", str(config), "--total-points", str(n), "--steps", "3", "--warmup", "3", "--e2e-steps", "2",
            "--no-cpu-baseline", "--verify"]
     r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
