@@ -20,6 +20,7 @@
 #include <stdexcept>
 #include <string>
 
+#include "chp/b200.hpp"
 #include "chp/geometry.hpp"
 #include "chp/hulls.hpp"
 #include "chp/kernels.hpp"
@@ -55,6 +56,72 @@ void check(int rc) {
     const std::string msg = chp_last_error(ctx());
     if (rc == CHP_EINVAL) throw std::invalid_argument(msg);
     throw std::runtime_error(msg);
+}
+
+// Multi-device reduce (chp/b200.hpp): the shard group of this host thread.
+struct GroupHolder {
+    std::vector<int> devices;
+    bool nccl = true;
+    bool configured = false;
+    chp_group* group = nullptr;
+    ~GroupHolder() {
+        if (group) chp_group_destroy(group);
+    }
+};
+
+GroupHolder& group_holder() {
+    thread_local GroupHolder h;
+    if (!h.configured) {
+        h.configured = true;
+        if (const char* env = std::getenv("CHP_DEVICES")) {
+            std::string s(env);
+            size_t pos = 0;
+            while (pos < s.size()) {
+                const size_t comma = s.find(',', pos);
+                const std::string tok = s.substr(pos, comma == std::string::npos ? std::string::npos : comma - pos);
+                if (!tok.empty()) h.devices.push_back(std::atoi(tok.c_str()));
+                if (comma == std::string::npos) break;
+                pos = comma + 1;
+            }
+        }
+        const char* comb = std::getenv("CHP_COMBINE");
+        h.nccl = !(comb && std::string(comb) == "peer");
+    }
+    return h;
+}
+
+// The group when more than one device is configured, else nullptr.
+chp_group* group() {
+    GroupHolder& h = group_holder();
+    if (h.devices.size() < 2) return nullptr;
+    if (!h.group) {
+        const int rc = chp_group_create(h.devices.data(), static_cast<int>(h.devices.size()),
+                                        h.nccl ? CHP_COMBINE_NCCL : CHP_COMBINE_PEER, &h.group);
+        if (rc == CHP_EINVAL) throw std::invalid_argument("chp: bad device list for the shard group");
+        if (rc != CHP_OK) throw std::runtime_error("chp: shard group creation failed");
+    }
+    return h.group;
+}
+
+void check_group(chp_group* g, int rc) {
+    if (rc == CHP_OK) return;
+    const std::string msg = chp_group_last_error(g);
+    if (rc == CHP_EINVAL) throw std::invalid_argument(msg);
+    throw std::runtime_error(msg);
+}
+
+// The chain reduce() computed alongside L (one device round trip less for
+// the usual reduce -> build_polyline sequence): build_polyline reuses it
+// when the array it is given still holds exactly that L with no offsets.
+struct ChainCache {
+    std::vector<int32_t> pairs;  // L in serialize form, as reduce() returned it
+    std::vector<int32_t> chain;  // its Lemma-1 chain (int32 x, y)
+    bool valid = false;
+};
+
+ChainCache& chain_cache() {
+    thread_local ChainCache c;
+    return c;
 }
 
 int32_t narrow1(std::int64_t v) {
@@ -290,10 +357,32 @@ ExtremalArray reduce(std::span<const Point> points, std::int64_t width, std::opt
     if (width < 1) throw std::invalid_argument("reduce: width must be >= 1");
     std::vector<int32_t> L(2 * static_cast<size_t>(width));
     std::vector<std::uint64_t> words((static_cast<size_t>(width) + 63) / 64);
-    int64_t s = 0;
+    detail::ChainCache& cache = detail::chain_cache();
+    cache.valid = false;
+    cache.chain.resize(4 * static_cast<size_t>(width));
+    int64_t s = -1;
     const int64_t qq = q ? std::max<int64_t>(*q, 0) : -1;
-    detail::check(chp_pipeline_host64(detail::ctx(), detail::raw64(points), points.size(), width, qq, L.data(),
-                                      words.data(), nullptr, &s, nullptr, nullptr));
+    chp_group* g = width <= (1ll << 29) ? detail::group() : nullptr;
+    const int rc = g ? chp_pipeline_host64_sharded(g, detail::raw64(points), points.size(), width, qq, L.data(),
+                                                   words.data(), cache.chain.data(), &s, nullptr, nullptr)
+                     : chp_pipeline_host64(detail::ctx(), detail::raw64(points), points.size(), width, qq, L.data(),
+                                           words.data(), cache.chain.data(), &s, nullptr, nullptr);
+    if (rc == CHP_EINVAL && s == 0) {
+        // valid input, no point at all: the pipeline refuses the (empty)
+        // chain it was asked for, and L is all sentinels
+        for (int64_t i = 0; i < width; ++i) {
+            L[2 * i] = detail::narrow1(width + 1);
+            L[2 * i + 1] = -1;
+        }
+        std::fill(words.begin(), words.end(), 0);
+    } else if (g) {
+        detail::check_group(g, rc);
+    } else {
+        detail::check(rc);
+    }
+    cache.chain.resize(2 * static_cast<size_t>(std::max<int64_t>(s, 0)));
+    cache.pairs = L;
+    cache.valid = true;
     ExtremalArray arr{detail::entries_from_pairs(L), occupancy::Index(static_cast<std::uint64_t>(width), occ_kind)};
     arr.occ.assign_words(words.data(), words.size());
     return arr;
@@ -326,6 +415,12 @@ ExtremalArray second_scan(const ExtremalArray& arr, occupancy::Kind occ_kind) {
 PolygonalChain build_polyline(const ExtremalArray& arr) {
     if (arr.width() < 1) throw std::invalid_argument("build_polyline: no valid points");
     const auto L = detail::pairs_from_entries(arr.entries);
+    const detail::ChainCache& cache = detail::chain_cache();
+    if (cache.valid && arr.major_offset == 0 && arr.minor_offset == 0 && !arr.axis_swapped && L == cache.pairs) {
+        // the L reduce() just produced: its chain came back with it
+        if (cache.chain.empty()) throw std::invalid_argument("build_polyline: no valid points");
+        return PolygonalChain{detail::widen(cache.chain.data(), static_cast<int64_t>(cache.chain.size() / 2))};
+    }
     std::vector<int32_t> chain(4 * L.size() / 2 + 4);
     int64_t s = 0;
     detail::check(chp_polyline_host(detail::ctx(), L.data(), arr.width(), arr.major_offset, arr.minor_offset,
@@ -420,4 +515,26 @@ Hull brute_force_hull(std::span<const Point> points, std::size_t max_points) {
 }
 
 }  // namespace hulls
+
+// ------------------------------------------------------ device options
+namespace b200 {
+
+void use_devices(const std::vector<int>& devs, bool nccl) {
+    detail::GroupHolder& h = detail::group_holder();
+    if (h.group) {
+        chp_group_destroy(h.group);
+        h.group = nullptr;
+    }
+    h.devices = devs;
+    h.nccl = nccl;
+}
+
+std::vector<int> devices() {
+    const detail::GroupHolder& h = detail::group_holder();
+    if (h.devices.size() >= 2) return h.devices;
+    const char* env = std::getenv("CHP_DEVICE");
+    return {env ? std::atoi(env) : 0};
+}
+
+}  // namespace b200
 }  // namespace chp

@@ -12,6 +12,7 @@
 #include <string>
 #include <vector>
 
+#include "chp/b200.hpp"
 #include "chp/geometry.hpp"
 #include "chp/hulls.hpp"
 #include "chp/kernels.hpp"
@@ -274,6 +275,50 @@ void acceptance_c3() {
     EXPECT(res.array.valid_count() == 2000);
 }
 
+void chain_reuse_and_devices() {
+    // build_polyline after reduce reuses the chain that came back with L; an
+    // array edited afterwards (or with offsets) takes the device round trip.
+    // Either way the chain is the Lemma-1 chain of the array it is given
+    // (test_reducer.cpp:188-207).
+    const auto a = reduce(five_columns(), 5);
+    const auto c1 = build_polyline(a);
+    EXPECT(c1.vertices.size() == 9);
+    EXPECT(c1.vertices.front() == (Point{1, 1}) && c1.vertices.back() == (Point{5, 3}));
+    auto b = a;
+    b.entries[0].hi = 7;  // edited after reduce: (1,1),(1,7) ...
+    const auto c2 = build_polyline(b);
+    EXPECT(c2.vertices.size() == 9 && c2.vertices[1] == (Point{1, 7}));
+    auto c = a;
+    c.major_offset = 10;  // offsets: to_original moves every point
+    EXPECT(build_polyline(c).vertices.front() == (Point{11, 1}));
+    // empty input: all slots empty, build_polyline throws (test_reducer.cpp:198-207)
+    const auto e = reduce(std::vector<Point>{}, 4);
+    EXPECT(e.valid_count() == 0);
+    EXPECT_THROWS(build_polyline(e), std::invalid_argument);
+    EXPECT(build_polyline(a).vertices == c1.vertices);
+
+    // reduce split over a shard group (chp/b200.hpp): four shards on the
+    // first device with the peer combine give the single-device result
+    std::mt19937_64 rng(11);
+    std::uniform_int_distribution<std::int64_t> dx(1, 3000), dy(1, 5000);
+    std::vector<Point> pts(2000003);
+    for (auto& q : pts) q = {dx(rng), dy(rng)};
+    const auto one = reduce(pts, 3000, 5000);
+    const auto chain_one = build_polyline(one);
+    const int dev = chp::b200::devices().front();
+    chp::b200::use_devices({dev, dev, dev, dev}, /*nccl=*/false);
+    EXPECT(chp::b200::devices().size() == 4);
+    const auto four = reduce(pts, 3000, 5000);
+    EXPECT(four.entries == one.entries);
+    EXPECT(build_polyline(four).vertices == chain_one.vertices);
+    auto bad = pts;
+    bad[2000000] = {3001, 1};  // in the last shard
+    EXPECT_THROWS(reduce(bad, 3000, 5000), std::invalid_argument);
+    chp::b200::use_devices({dev});
+    EXPECT(chp::b200::devices().size() == 1);
+    EXPECT(reduce(pts, 3000, 5000).entries == one.entries);
+}
+
 }  // namespace
 
 int main() {
@@ -282,6 +327,7 @@ int main() {
     occupancy_kats();
     kernel_kats();
     acceptance_c3();
+    chain_reuse_and_devices();
     std::printf("%d checks, %d failed\n", g_checks, g_fail);
     return g_fail ? 1 : 0;
 }
