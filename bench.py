@@ -459,7 +459,8 @@ class Arm:
         path = ("chp_pipeline_host" if self.world == 1 else
                 "per rank chp_reduce_host on its slice, NCCL MIN all-reduce of L, rank 0 chp_finish_host") + \
                " (pinned int32 input; " + \
-               (("8 Mi-point chunks packed to 16-bit slot|y words" if p <= 65536 else
+               (("8 Mi-point chunks packed to 2-byte slot|y points (8 bits each)" if p <= 256 else
+                 "8 Mi-point chunks packed to 16-bit slot|y words" if p <= 65536 else
                  "8 Mi-point chunks packed to 42-bit slot|y points, 3 per 16 bytes")
                 + " on host threads, int32 chunks DMA'd from the input's end while the host packs, "
                 if packed else "16 Mi-point int32 chunks, ") + "H2D overlapped with K1)"
@@ -486,8 +487,8 @@ class Arm:
         return {"value": n_total / (pre_ms * 1e-3) / 1e9, "unit": "Gpoints/s", "ms_per_step": pre_ms,
                 "h2d_bytes_per_step": self.ctx.last_h2d_bytes,
                 "path": "chp_precondition_run + chp_last_outputs (pinned int32 input, bounds unknown: one pass, "
-                        "speculative 16-bit (or 42-bit) packing against a 2^16 (2^21) window from a 64 Ki-point "
-                        "prefix, the bounds folded as the chunks land)"}
+                        "speculative 2-byte, 4-byte or 42-bit packing against a 2^8, 2^16 or 2^21 window from a "
+                        "64 Ki-point prefix, the bounds folded as the chunks land)"}
 
 
 def main():

@@ -327,6 +327,67 @@ uint32_t pack_any(const HostPts& in, uint64_t off, uint64_t m, uint32_t* __restr
     return bad;
 }
 
+// 8-bit packing (width and y range up to 2^8 each, e.g. C5's 256 x 256):
+// v = slot | (y - ybase) << 8 as uint16, eight points per 16-byte word, 2
+// bytes per point instead of 8 (k_unpack8 in misc.cu).  16 points per AVX2
+// step: the (x, y) lanes are split, range-checked and combined as in
+// pack16_avx2, then two 8 x 32-bit vectors narrow to one 16 x 16-bit store
+// (packus saturates only invalid points, which are flagged anyway).
+__attribute__((target("avx2"))) uint32_t pack8_avx2(const int32_t* __restrict__ src, uint16_t* __restrict__ dst,
+                                                    uint64_t m, uint32_t base, uint32_t ybase, uint32_t wcheck,
+                                                    uint32_t qmax) {
+    uint64_t i = 0;
+    uint32_t bad = 0;
+    auto one = [&](uint64_t k) {
+        const uint32_t s = (uint32_t)src[2 * k] - base;
+        const uint32_t t = (uint32_t)src[2 * k + 1] - ybase;
+        bad |= (uint32_t)(s >= wcheck) | (uint32_t)(t >= qmax);
+        dst[k] = (uint16_t)((s & 0xFFu) | ((t & 0xFFu) << 8));
+    };
+    for (; i < m && (reinterpret_cast<uintptr_t>(dst + i) & 31); ++i) one(i);
+    const __m256i vbase = _mm256_set1_epi32((int)base), vone = _mm256_set1_epi32((int)ybase);
+    const __m256i wl = _mm256_set1_epi32((int)wcheck), ql = _mm256_set1_epi32((int)qmax);
+    const __m256i perm = _mm256_setr_epi32(0, 2, 4, 6, 1, 3, 5, 7);
+    __m256i badv = _mm256_setzero_si256();
+    for (; i + 16 <= m; i += 16) {
+        const __m256i* p = reinterpret_cast<const __m256i*>(src + 2 * i);
+        const __m256i a = _mm256_permutevar8x32_epi32(_mm256_loadu_si256(p), perm);
+        const __m256i b = _mm256_permutevar8x32_epi32(_mm256_loadu_si256(p + 1), perm);
+        const __m256i c = _mm256_permutevar8x32_epi32(_mm256_loadu_si256(p + 2), perm);
+        const __m256i d = _mm256_permutevar8x32_epi32(_mm256_loadu_si256(p + 3), perm);
+        const __m256i s0 = _mm256_sub_epi32(_mm256_permute2x128_si256(a, b, 0x20), vbase);
+        const __m256i t0 = _mm256_sub_epi32(_mm256_permute2x128_si256(a, b, 0x31), vone);
+        const __m256i s1 = _mm256_sub_epi32(_mm256_permute2x128_si256(c, d, 0x20), vbase);
+        const __m256i t1 = _mm256_sub_epi32(_mm256_permute2x128_si256(c, d, 0x31), vone);
+        badv = _mm256_or_si256(badv, _mm256_cmpeq_epi32(_mm256_max_epu32(s0, wl), s0));
+        badv = _mm256_or_si256(badv, _mm256_cmpeq_epi32(_mm256_max_epu32(t0, ql), t0));
+        badv = _mm256_or_si256(badv, _mm256_cmpeq_epi32(_mm256_max_epu32(s1, wl), s1));
+        badv = _mm256_or_si256(badv, _mm256_cmpeq_epi32(_mm256_max_epu32(t1, ql), t1));
+        const __m256i w0 = _mm256_or_si256(s0, _mm256_slli_epi32(t0, 8));
+        const __m256i w1 = _mm256_or_si256(s1, _mm256_slli_epi32(t1, 8));
+        // packus: [w0 0-3 | w1 0-3 | w0 4-7 | w1 4-7] -> qwords 0, 2, 1, 3
+        const __m256i pk = _mm256_permute4x64_epi64(_mm256_packus_epi32(w0, w1), 0xD8);
+        _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + i), pk);
+    }
+    for (; i < m; ++i) one(i);
+    _mm_sfence();
+    return bad | (uint32_t)!_mm256_testz_si256(badv, badv);
+}
+
+uint32_t pack8_any(const HostPts& in, uint64_t off, uint64_t m, uint16_t* __restrict__ dst, uint32_t base,
+                   uint32_t ybase, uint32_t wcheck, uint32_t qmax) {
+    static const bool avx2 = __builtin_cpu_supports("avx2");
+    if (in.p32 && avx2) return pack8_avx2(in.p32 + 2 * off, dst, m, base, ybase, wcheck, qmax);
+    const int64_t b64 = (int32_t)base, y64 = (int32_t)ybase;
+    uint32_t bad = 0;
+    for (uint64_t k = 0; k < m; ++k) {
+        const int64_t s = in.x(off + k) - b64, t = in.y(off + k) - y64;
+        bad |= (uint32_t)((uint64_t)s >= wcheck) | (uint32_t)((uint64_t)t >= qmax);
+        dst[k] = (uint16_t)(((uint32_t)s & 0xFFu) | (((uint32_t)t & 0xFFu) << 8));
+    }
+    return bad;
+}
+
 // 42-bit packing (width and y range up to 2^21 each, e.g. C4's 2^20 x 2^20):
 // v = slot | (y - ybase) << 21, three points per 16-byte word (lo64 = v0 |
 // v1 << 42, hi64 = v1 >> 22 | v2 << 20; k_unpack42 in misc.cu), 5.33 bytes
@@ -376,18 +437,26 @@ uint32_t pack42_any(const HostPts& in, uint64_t off, uint64_t m, uint64_t* __res
 // DMA'd straight from the END of the input (K1 validates those itself), so
 // the packed front and the raw back meet where both resources finish.
 //
-// wide = true: the 42-bit form (three points per 16-byte word) for ranges up
-// to 2^21 x 2^21 (not speculative).
+// mode: kPack16 (4 bytes per point), kPack42 (three points per 16-byte word,
+// ranges up to 2^21 x 2^21), kPack8 (2 bytes per point, ranges up to
+// 2^8 x 2^8).  Each is used both for known ranges (reduce with q given) and
+// speculatively against a window (reduce with q unset: kPack16;
+// precondition: the window its input's prefix fits, any mode): a chunk that
+// fails the window check then travels as int32 pairs (send_raw).
+enum PackMode { kPack16 = 0, kPack42 = 1, kPack8 = 2 };
 template <typename Launch>
 int stream_chunks_packed(chp_ctx* ctx, const HostPts& in, uint64_t n, int64_t x_off, int32_t ybase,
                          uint32_t wcheck, uint32_t qmax, bool speculative, bool* bad, Launch&& launch,
-                         int32_t* d_dest = nullptr, bool wide = false) {
+                         int32_t* d_dest = nullptr, int mode = kPack16) {
     *bad = false;
     if (n == 0) return CHP_OK;
+    const bool wide = mode == kPack42;
     // packed bytes of m points; part boundaries within a chunk keep whole words
-    auto pbytes = [&](uint64_t m) -> uint64_t { return wide ? (m + 2) / 3 * 16 : m * 4; };
-    const uint64_t align = wide ? 24 : 8;
-    double& rate = wide ? ctx->pack_rate42 : ctx->pack_rate;
+    auto pbytes = [&](uint64_t m) -> uint64_t {
+        return wide ? (m + 2) / 3 * 16 : mode == kPack8 ? (m + 7) / 8 * 16 : m * 4;
+    };
+    const uint64_t align = wide ? 24 : 16;
+    double& rate = wide ? ctx->pack_rate42 : mode == kPack8 ? ctx->pack_rate8 : ctx->pack_rate;
     // 8 Mi points per chunk (e2e C2, hybrid: 2 Mi 8.7-9.1, 4 Mi 9.4-9.7, 8 Mi
     // 9.9, 16 Mi 10.0 Gpts/s; smaller chunks pay the per-chunk dispatch).
     constexpr uint64_t kPackChunk = 8ull << 20;
@@ -494,6 +563,7 @@ int stream_chunks_packed(chp_ctx* ctx, const HostPts& in, uint64_t n, int64_t x_
         CHP_CUDA(ctx, cudaEventSynchronize(ctx->ev_copied[b]));
         uint32_t* dst = static_cast<uint32_t*>(ctx->pack_host[b]);
         uint64_t* dst64 = static_cast<uint64_t*>(ctx->pack_host[b]);
+        uint16_t* dst16 = static_cast<uint16_t*>(ctx->pack_host[b]);
         const int parts = pool->parts_for(mm);
         const auto t0 = std::chrono::steady_clock::now();
         std::fill(part_bad.begin(), part_bad.end(), 0u);
@@ -503,7 +573,9 @@ int stream_chunks_packed(chp_ctx* ctx, const HostPts& in, uint64_t n, int64_t x_
                 const uint64_t hi = i + 1 == parts ? mm : mm * (uint64_t)(i + 1) / parts / align * align;
                 part_bad[(size_t)i] =
                     wide ? pack42_any(in, front + lo, hi - lo, dst64 + 2 * (lo / 3), base, (uint32_t)ybase, wcheck, qmax)
-                         : pack_any(in, front + lo, hi - lo, dst + lo, base, (uint32_t)ybase, wcheck, qmax);
+                    : mode == kPack8
+                        ? pack8_any(in, front + lo, hi - lo, dst16 + lo, base, (uint32_t)ybase, wcheck, qmax)
+                        : pack_any(in, front + lo, hi - lo, dst + lo, base, (uint32_t)ybase, wcheck, qmax);
             },
             parts);
         const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -526,7 +598,9 @@ int stream_chunks_packed(chp_ctx* ctx, const HostPts& in, uint64_t n, int64_t x_
         CHP_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_copied[b], 0));
         int32_t* udst = d_dest ? d_dest + 2 * front : (int32_t*)ctx->unpack_dev[b].p;
         if ((rc = wide ? chp_unpack42(ctx, ctx->stage_dev[b].p, mm, (int32_t)base, ybase, udst)
-                       : chp_unpack16(ctx, (const uint32_t*)ctx->stage_dev[b].p, mm, (int32_t)base, ybase, udst)))
+                  : mode == kPack8 ? chp_unpack8(ctx, ctx->stage_dev[b].p, mm, (int32_t)base, ybase, udst)
+                                   : chp_unpack16(ctx, (const uint32_t*)ctx->stage_dev[b].p, mm, (int32_t)base,
+                                                  ybase, udst)))
             return rc;
         CHP_CUDA(ctx, cudaEventRecord(ctx->ev_consumed[b], ctx->stream));
         if ((rc = launch(d_dest ? (const int32_t*)(d_dest + 2 * front) : (const int32_t*)ctx->unpack_dev[b].p, mm)))
@@ -587,6 +661,8 @@ int stream_reduce(chp_ctx* ctx, const HostPts& in, uint64_t n, int64_t width, in
                             !(flags & CHP_REDUCE_NO_VALIDATE) && !(flags & CHP_PIPELINE_NO_PACK) &&
                             !std::getenv("CHP_PIPELINE_NO_PACK") && x_off + 1 >= (int64_t)INT32_MIN &&
                             x_off <= (int64_t)INT32_MAX && ybase >= (int64_t)INT32_MIN && ybase <= (int64_t)INT32_MAX;
+    // Known ranges up to 2^8 x 2^8 (e.g. C5: 256 x 256): 2 bytes per point.
+    const bool packable8 = packable && !speculative && width <= 256 && ycount <= 256;
     bool bad = false;
     int rc;
     if (!packable && !packable42) {
@@ -598,7 +674,7 @@ int stream_reduce(chp_ctx* ctx, const HostPts& in, uint64_t n, int64_t width, in
         const uint32_t qmax =
             (uint32_t)std::min<int64_t>(speculative ? 65536 : ycount, (int64_t)INT32_MAX - ybase + 1);
         if ((rc = stream_chunks_packed(ctx, in, n, x_off, (int32_t)ybase, wcheck, qmax, speculative, &bad, launch,
-                                       nullptr, packable42)))
+                                       nullptr, packable8 ? kPack8 : packable42 ? kPack42 : kPack16)))
             return rc;
     }
     if (bad) {  // same outcome as the unpacked path: the error word of DL
@@ -939,13 +1015,15 @@ static int precondition_core(chp_ctx* ctx, const HostPts& in, uint64_t n, int64_
         // A prefix wider than 2^16 tries a 2^21 window and the 42-bit form.
         int64_t wx = 0, wy = 0;
         const bool pack = !std::getenv("CHP_PIPELINE_NO_PACK");
-        const bool win = pack && pack_window(ctx, in, n, &wx, &wy);
-        const bool win42 = pack && !win && pack_window(ctx, in, n, &wx, &wy, 1 << 21);
+        // A prefix within 2^8 x 2^8 tries a 2^8 window and 2 bytes per point.
+        const bool win8 = pack && pack_window(ctx, in, n, &wx, &wy, 256);
+        const bool win = pack && !win8 && pack_window(ctx, in, n, &wx, &wy);
+        const bool win42 = pack && !win8 && !win && pack_window(ctx, in, n, &wx, &wy, 1 << 21);
         bool narrow_bad = false;  // int64 input: a coordinate beyond int32
-        if (win || win42) {
-            const uint32_t W = win ? 65536u : (1u << 21);
+        if (win8 || win || win42) {
+            const uint32_t W = win8 ? 256u : win ? 65536u : (1u << 21);
             if ((rc = stream_chunks_packed(ctx, in, n, wx - 1, (int32_t)wy, W, W, true, &narrow_bad, fold,
-                                           (int32_t*)pts.p, win42)))
+                                           (int32_t*)pts.p, win8 ? kPack8 : win42 ? kPack42 : kPack16)))
                 return rc;
         } else {
             uint32_t nb = 0;

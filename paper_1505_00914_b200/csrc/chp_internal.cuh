@@ -9,6 +9,7 @@
 #include <string>
 #include <unordered_map>
 #include <utility>
+#include <vector>
 
 #include "chp_b200.h"
 
@@ -69,10 +70,23 @@ struct chp_ctx {
     cudaEvent_t ev_rconsumed[2] = {nullptr, nullptr};
     double pack_rate = 8e9;    // points / s, 16-bit packing
     double pack_rate42 = 6e9;  // points / s, 42-bit packing
+    double pack_rate8 = 8e9;   // points / s, 8-bit packing
     // Launch-setup cache (reduce.cu kernel_blocks): kernel -> (dynamic smem
     // it was configured for, resident blocks per SM at that size).
     std::unordered_map<const void*, std::pair<size_t, int>> kcache;
+    // Diagnostics (chp_debug_trace_*; not in the header): an event recorded
+    // on the stream at each traced point of K1's launch sequence.
+    bool tracing = false;
+    std::vector<std::pair<cudaEvent_t, const char*>> trace;
 };
+
+static inline void chp_trace(chp_ctx* ctx, const char* what) {
+    if (!ctx->tracing) return;
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    cudaEventRecord(e, ctx->stream);
+    ctx->trace.emplace_back(e, what);
+}
 
 // Record the first CUDA error of a launch sequence in ctx->err.
 static inline int chp_cuda_fail(chp_ctx* ctx, cudaError_t e, const char* what) {
@@ -117,6 +131,8 @@ int chp_bounds_accumulate(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int32_t
 // Packed host pipeline (abi.cu): 32-bit words (slot | (y - 1) << 16) back to
 // int32 (x, y) pairs with x = slot + base.
 int chp_unpack16(chp_ctx* ctx, const uint32_t* d_in, uint64_t n, int32_t base, int32_t ybase, int32_t* d_out);
+// The same for 16-bit points (slot | (y - ybase) << 8), eight per 16-byte word.
+int chp_unpack8(chp_ctx* ctx, const void* d_in, uint64_t n, int32_t base, int32_t ybase, int32_t* d_out);
 // The same for 42-bit points (slot | (y - ybase) << 21), three per 16-byte word.
 int chp_unpack42(chp_ctx* ctx, const void* d_in, uint64_t n, int32_t base, int32_t ybase, int32_t* d_out);
 // K1 with a general valid y range [ybase, ybase + ycount) (reduce.cu).

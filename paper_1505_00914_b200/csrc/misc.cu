@@ -164,7 +164,49 @@ __global__ void k_unpack42(const uint4* __restrict__ in, uint64_t n, int32_t bas
         }
     }
 }
+// 16-bit form for ranges up to 2^8 x 2^8: point v = slot | (y - ybase) << 8,
+// eight per 16-byte word -> four 16-byte stores.
+__global__ void k_unpack8(const uint4* __restrict__ in8, uint64_t n, int32_t base, int32_t ybase,
+                          int4* __restrict__ out4, int2* __restrict__ out, int vec) {
+    const uint64_t nw = n / 8;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nw; i += stride) {
+        const uint4 q = __ldcs(in8 + i);
+        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+        int v[16];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            v[4 * k] = (int)(w[k] & 0xFFu) + base;
+            v[4 * k + 1] = (int)((w[k] >> 8) & 0xFFu) + ybase;
+            v[4 * k + 2] = (int)((w[k] >> 16) & 0xFFu) + base;
+            v[4 * k + 3] = (int)(w[k] >> 24) + ybase;
+        }
+        if (vec) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) out4[4 * i + k] = make_int4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) out[8 * i + k] = make_int2(v[2 * k], v[2 * k + 1]);
+        }
+    }
+    if (blockIdx.x == 0) {
+        const uint16_t* in16 = reinterpret_cast<const uint16_t*>(in8);
+        for (uint64_t j = 8 * nw + threadIdx.x; j < n; j += blockDim.x)
+            out[j] = make_int2((int)(in16[j] & 0xFFu) + base, (int)(in16[j] >> 8) + ybase);
+    }
+}
 }  // namespace
+
+int chp_unpack8(chp_ctx* ctx, const void* d_in, uint64_t n, int32_t base, int32_t ybase, int32_t* d_out) {
+    if (n == 0) return CHP_OK;
+    const uint64_t nw = n / 8;
+    const int vec = (reinterpret_cast<uintptr_t>(d_out) & 15) == 0;
+    const int blocks = (int)std::min<uint64_t>((nw + 255) / 256 + 1, (uint64_t)ctx->sm_count * 8);
+    k_unpack8<<<blocks, 256, 0, ctx->stream>>>(reinterpret_cast<const uint4*>(d_in), n, base, ybase,
+                                               reinterpret_cast<int4*>(d_out), reinterpret_cast<int2*>(d_out), vec);
+    CHP_LAUNCHED(ctx);
+    return CHP_OK;
+}
 
 int chp_unpack42(chp_ctx* ctx, const void* d_in, uint64_t n, int32_t base, int32_t ybase, int32_t* d_out) {
     if (n == 0) return CHP_OK;

@@ -1387,16 +1387,20 @@ int run_group_filter(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, const Geo& g
     const uint32_t kw = kfield ? kfield + 3 : 6;
     // (Inputs under 4 Mi points: one pass with the empty table.)
     const uint64_t warm = n < (1ull << 22) ? n : (n >> kw) & ~1ull;
+    chp_trace(ctx, "filter:warm");
     if ((rc = pass(d_xy, warm, nullptr))) return rc;
     for (uint64_t done = warm; done < n;) {
+        chp_trace(ctx, "filter:build");
         k_filter_build<W><<<(ngroups + 1 + 255) / 256, 256, 0, ctx->stream>>>(d_L, w, gshift, (int32_t)g.ybase,
                                                                             ys, (W*)ctx->filter.p, ngroups, qs);
         CHP_LAUNCHED(ctx);
         const uint64_t stop = std::min<uint64_t>(n, 2 * done);
         cur_done = done;
+        chp_trace(ctx, "filter:phase");
         if ((rc = pass(d_xy + 2 * done, stop - done, (const W*)ctx->filter.p))) return rc;
         done = stop;
     }
+    chp_trace(ctx, "filter:end");
     return CHP_OK;
 }
 
@@ -1596,6 +1600,7 @@ int chp_reduce_yr(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t width, 
                     // shared and the grid cannot be co-resident: then the
                     // split form below runs instead.)
                     static const bool refuse = getenv("CHP_TEST_COOP_REFUSE") != nullptr;  // tests
+                    chp_trace(ctx, "sampled:sample+merge");
                     const cudaError_t ce = cudaLaunchCooperativeKernel(fused, dim3(sblocks * (refuse ? 64 : 1)),
                                                                        dim3(kThreads), args, smem, ctx->stream);
                     if (ce != cudaSuccess) {
@@ -1608,6 +1613,7 @@ int chp_reduce_yr(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t width, 
                         return CHP_OK;
                     }
                     const Plan pl = plan_for(ctx, tbytes, flags, false);
+                    chp_trace(ctx, "sampled:main");
                     if (yknown)
                         CHP_LAUNCH_PLANNED_PDL(ctx, pl, (k_reduce_sampled<true, false>),
                                                (k_reduce_sampled<false, false>), d_xy, n, g, w, wpad8, qz, qpart,
@@ -1676,6 +1682,34 @@ int chp_reduce_yr(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t width, 
 extern "C" int chp_reduce(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t width, int64_t q,
                           int64_t x_off, int32_t* d_L, uint32_t flags) {
     return chp_reduce_yr(ctx, d_xy, n, width, 1, q, x_off, d_L, flags);
+}
+
+// Diagnostics, not part of include/chp_b200.h (tools/trace_k1.py).
+extern "C" int chp_debug_trace_enable(chp_ctx* ctx, int on) {
+    if (!ctx) return CHP_EINVAL;
+    for (auto& t : ctx->trace) cudaEventDestroy(t.first);
+    ctx->trace.clear();
+    ctx->tracing = on != 0;
+    return CHP_OK;
+}
+
+extern "C" int chp_debug_trace_mark(chp_ctx* ctx, const char* label) {
+    if (!ctx) return CHP_EINVAL;
+    chp_trace(ctx, label);
+    return CHP_OK;
+}
+
+// ms[i] = time from trace point i to i + 1; labels[i] its label.  Returns the
+// number of intervals written.
+extern "C" int chp_debug_trace_read(chp_ctx* ctx, float* ms, const char** labels, int cap) {
+    if (!ctx) return -1;
+    cudaStreamSynchronize(ctx->stream);
+    int k = 0;
+    for (size_t i = 0; i + 1 < ctx->trace.size() && k < cap; ++i, ++k) {
+        cudaEventElapsedTime(&ms[k], ctx->trace[i].first, ctx->trace[i + 1].first);
+        labels[k] = ctx->trace[i].second;
+    }
+    return k;
 }
 
 extern "C" int chp_check(chp_ctx* ctx, const int32_t* d_L, int64_t width) {

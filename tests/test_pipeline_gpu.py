@@ -281,3 +281,81 @@ def test_precondition_speculative_window42(ctx, orc, pinned):
     assert out["bbox"] == ref["bbox"]
     assert np.array_equal(out["chain"], ref["chain"])
     assert np.array_equal(out["hull"], ref["hull"])
+
+
+# Known ranges up to 2^8 x 2^8 (C5: 256 x 256) travel as 16-bit points,
+# eight per 16 bytes (2 bytes per point instead of 8).
+def _packed8_bytes(n, chunk=8 << 20):
+    return sum((min(chunk, n - a) + 7) // 8 * 16 for a in range(0, n, chunk))
+
+
+@pytest.mark.parametrize("n", [1, 7, 8, 9, 15, 16, 17, 1001, 8_388_608 + 13, 20_000_001])
+@pytest.mark.parametrize("pinned", [False, True])
+def test_pipeline_host_packed8(ctx, orc, n, pinned):
+    p = 256
+    xy = generate_host(5, 5, p, n)
+    if pinned:
+        xy = _pinned(xy)
+    out = ctx.pipeline_host(xy, p, p, L=True, chain=True, hull=True)
+    if pinned:  # (part of it goes as int32 pairs from the end)
+        assert 2 * n <= ctx.last_h2d_bytes <= 8 * n + 16
+    else:
+        assert ctx.last_h2d_bytes == _packed8_bytes(n)
+    ref = orc.pipeline(xy, p, p)
+    assert np.array_equal(out["L"], ref["L"])
+    assert np.array_equal(out["chain"], ref["chain"])
+    assert np.array_equal(out["hull"], ref["hull"])
+
+
+def test_pipeline_host_packed8_extremes(ctx, orc):
+    # the 8-bit fields at both ends, in every position of a 16-point AVX2 step
+    p, q = 256, 256
+    base = np.array([[1, 1], [1, q], [p, 1], [p, q], [100, 7], [p - 1, q - 1], [2, 2]], np.int32)
+    for shift in range(17):
+        xy = np.concatenate([np.full((shift, 2), 5, np.int32), np.repeat(base, 37, axis=0)])
+        out = ctx.pipeline_host(xy, p, q, L=True, chain=True)
+        ref = orc.pipeline(xy, p, q)
+        assert np.array_equal(out["L"], ref["L"])
+        assert np.array_equal(out["chain"], ref["chain"])
+    # a narrower box inside the 8-bit window (w = 100, q = 37)
+    xy = np.stack([np.arange(1, 10_001) % 100 + 1, np.arange(10_000) % 37 + 1], axis=1).astype(np.int32)
+    out = ctx.pipeline_host(xy, 100, 37, L=True, chain=True)
+    ref = orc.pipeline(xy, 100, 37)
+    assert np.array_equal(out["L"], ref["L"]) and np.array_equal(out["chain"], ref["chain"])
+
+
+@pytest.mark.parametrize("bad", [(0, 5), (257, 5), (7, 0), (7, 257), (-2**31, 1), (2**31 - 1, 2**31 - 1)])
+@pytest.mark.parametrize("where", [0, 15, 16, 999_999])
+@pytest.mark.parametrize("pinned", [False, True])
+def test_pipeline_host_packed8_invalid_raises(ctx, bad, where, pinned):
+    p = 256
+    xy = generate_host(5, 5, p, 1_000_000)
+    if pinned:
+        xy = _pinned(xy)
+    xy[where] = bad
+    with pytest.raises(ValueError):
+        ctx.pipeline_host(xy, p, p)
+    xy[where] = (1, 1)
+    ctx.pipeline_host(xy, p, p)
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_precondition_speculative_window8(ctx, orc, pinned):
+    # A prefix within 256 x 256 takes a 2^8 window and 2 bytes per point; a
+    # later chunk that leaves it goes as int32 pairs, and its points count.
+    rng = np.random.default_rng(79)
+    n = 20_000_000
+    xy = np.empty((n, 2), np.int32)
+    xy[:, 0] = rng.integers(-5000, -4800, n)
+    xy[:, 1] = rng.integers(70_000, 70_250, n)
+    xy[17_000_000, 1] = 80_000  # outside the window: that chunk is sent unpacked
+    if pinned:
+        xy = _pinned(xy)
+    out = ctx.precondition_host(xy, chain=True, hull=True)
+    if not pinned:
+        c = 8 << 20
+        assert ctx.last_h2d_bytes == _packed8_bytes(n) - _packed8_bytes(min(c, n - 2 * c)) + 8 * (n - 2 * c)
+    ref = orc.precondition(xy)
+    assert out["bbox"] == ref["bbox"]
+    assert np.array_equal(out["chain"], ref["chain"])
+    assert np.array_equal(out["hull"], ref["hull"])
