@@ -6,7 +6,7 @@
 // (src/reducer.cpp:42-49) and serialize's (width+1,-1) form (:121-130).
 //
 // One pass over the 8-byte slots with a single-pass decoupled look-back scan
-// (tiles of 2048 slots, 256 threads x 8 slots, dynamic tile order so every
+// (tiles of 128 threads x 4 or 16 slots, tile order such that every
 // predecessor of a tile has started).  The scanned value packs two counters
 // in a u64: c = 1 + [hi != lo] per valid slot (chain positions, Lemma-1
 // order) in the low word and v = [valid] (lower/upper positions) in the high
@@ -20,12 +20,12 @@
 
 namespace {
 
-// 128 threads x 4 slots: 512-slot tiles, so p = 65536 spreads over 128 CTAs
-// (2048-slot tiles left 32 CTAs latency-bound: 10.5 us at C2).
-constexpr int kCT = 128;       // threads per tile
-constexpr int kItems = 4;      // slots per thread
-constexpr int kLanesPerWord = 64 / kItems;
-constexpr int kTile = kCT * kItems;
+// 128 threads x ITEMS slots per tile.  ITEMS = 4 (512-slot tiles) up to
+// 2^17 slots, so p = 65536 spreads over 128 CTAs (2048-slot tiles left 32
+// CTAs latency-bound: 10.5 us at C2); ITEMS = 16 (2048-slot tiles) beyond,
+// so the look-back chain of p = 2^20 is 512 tiles long instead of 2048.
+constexpr int kCT = 128;  // threads per tile
+constexpr uint32_t kSmallTileMax = 1u << 17;
 
 constexpr unsigned long long kFlagAgg = 1ull << 62;
 constexpr unsigned long long kFlagIncl = 2ull << 62;
@@ -59,6 +59,7 @@ __device__ __forceinline__ int2 to_original(const Map& m, long long slot1, long 
     return m.swapped ? make_int2(minor, major) : make_int2(major, minor);
 }
 
+template <int kItems>
 __global__ void __launch_bounds__(kCT) k_compact(const int* __restrict__ DL, uint32_t width, Map map,
                                                  int2* __restrict__ chain, unsigned long long* __restrict__ occ,
                                                  int2* __restrict__ lpairs, int2* __restrict__ lower,
@@ -67,6 +68,8 @@ __global__ void __launch_bounds__(kCT) k_compact(const int* __restrict__ DL, uin
                                                  unsigned long long* __restrict__ status,
                                                  unsigned long long* __restrict__ status_next, uint32_t ntiles,
                                                  int use_ticket) {
+    constexpr int kLanesPerWord = 64 / kItems;
+    constexpr int kTile = kCT * kItems;
     __shared__ uint32_t s_tile;
     __shared__ unsigned long long s_warp[kCT / 32];
     __shared__ unsigned long long s_excl;
@@ -93,16 +96,34 @@ __global__ void __launch_bounds__(kCT) k_compact(const int* __restrict__ DL, uin
 
     int lo[kItems], hi[kItems];
     uint32_t vmask = 0, dmask = 0;
+    if (slot0 + kItems <= width && !(reinterpret_cast<uintptr_t>(DL) & 15)) {
+        // whole thread in range: 16-byte loads, all in flight together
+        const int4* g4 = reinterpret_cast<const int4*>(gL + slot0);
+        int4 q[kItems / 2];
+#pragma unroll
+        for (int j = 0; j < kItems / 2; ++j) q[j] = g4[j];  // (L1: the lane's later loads hit its sectors)
+#pragma unroll
+        for (int j = 0; j < kItems / 2; ++j) {
+            lo[2 * j] = q[j].x;
+            hi[2 * j] = ~q[j].y;
+            lo[2 * j + 1] = q[j].z;
+            hi[2 * j + 1] = ~q[j].w;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < kItems; ++j) {
+            const uint64_t s = slot0 + j;
+            lo[j] = CHP_EMPTY;
+            hi[j] = INT_MIN;
+            if (s < width) {
+                const int2 e = gL[s];
+                lo[j] = e.x;
+                hi[j] = ~e.y;
+            }
+        }
+    }
 #pragma unroll
     for (int j = 0; j < kItems; ++j) {
-        const uint64_t s = slot0 + j;
-        lo[j] = CHP_EMPTY;
-        hi[j] = INT_MIN;
-        if (s < width) {
-            const int2 e = gL[s];
-            lo[j] = e.x;
-            hi[j] = ~e.y;
-        }
         if (lo[j] <= hi[j]) {
             vmask |= 1u << j;
             if (lo[j] != hi[j]) dmask |= 1u << j;
@@ -193,29 +214,64 @@ __global__ void __launch_bounds__(kCT) k_compact(const int* __restrict__ DL, uin
         if (lane == 0) s_excl = excl;
     }
     __syncthreads();
-    const unsigned long long pre = s_excl + thread_excl;
-    uint32_t C = (uint32_t)pre;          // chain position (Lemma-1 order)
-    uint32_t V = (uint32_t)(pre >> 32);  // valid-slot position
+    const unsigned long long tile_pre = s_excl;
+    const unsigned long long pre = tile_pre + thread_excl;
+    const uint32_t C0 = (uint32_t)tile_pre, V0 = (uint32_t)(tile_pre >> 32);  // the tile's first positions
+    const uint32_t tileC = (uint32_t)tile_agg, tileV = (uint32_t)(tile_agg >> 32);
+    const uint64_t tile_slot0 = (uint64_t)tile * kTile;
+    const uint32_t tile_slots = (uint32_t)(width - tile_slot0 < (uint64_t)kTile ? width - tile_slot0 : kTile);
 
+    // Outputs go through a shared-memory stage, one output at a time, and
+    // leave the tile as contiguous runs: written straight from registers,
+    // each warp store touched 32 sectors for 8 bytes apiece (ncu, C4: 2.1 M
+    // store sectors for 16 MB of chain, 31 sectors per request).
+    extern __shared__ int2 stage[];  // 2 * kTile points
+    auto flush = [&](int2* __restrict__ dst, uint32_t count) {
+        __syncthreads();
+        for (uint32_t k = threadIdx.x; k < count; k += kCT) dst[k] = stage[k];
+        __syncthreads();
+    };
+    const uint32_t cl = (uint32_t)thread_excl, vl = (uint32_t)(thread_excl >> 32);  // local positions
+    if (chain) {
+        uint32_t c = cl;
 #pragma unroll
-    for (int j = 0; j < kItems; ++j) {
-        const uint64_t s = slot0 + j;
-        if (s >= width) break;
-        const bool v = (vmask >> j) & 1, d = (dmask >> j) & 1;
-        if (lpairs) lpairs[s] = v ? make_int2(lo[j], hi[j]) : make_int2((int)(width + 1), -1);
-        if (!v) continue;
-        const long long slot1 = (long long)s + 1;
-        if (chain) {
-            chain[C] = to_original(map, slot1, lo[j]);
-            if (d) chain[C + 1] = to_original(map, slot1, hi[j]);
+        for (int j = 0; j < kItems; ++j) {
+            if (!((vmask >> j) & 1)) continue;
+            const long long slot1 = (long long)(slot0 + j) + 1;
+            stage[c] = to_original(map, slot1, lo[j]);
+            if ((dmask >> j) & 1) stage[c + 1] = to_original(map, slot1, hi[j]);
+            c += ((dmask >> j) & 1) ? 2 : 1;
         }
-        const int32_t major = (int32_t)(slot1 + map.major_off);
-        if (lower) lower[V] = make_int2(major, (int32_t)(lo[j] + map.minor_off));
-        if (upper) upper[V] = make_int2(major, (int32_t)(hi[j] + map.minor_off));
-        if (upperd && d) upperd[C - V] = make_int2(major, (int32_t)(hi[j] + map.minor_off));
-        C += d ? 2 : 1;
-        V += 1;
+        flush(chain + C0, tileC);
     }
+    if (lpairs) {
+#pragma unroll
+        for (int j = 0; j < kItems; ++j)
+            stage[threadIdx.x * kItems + j] =
+                ((vmask >> j) & 1) ? make_int2(lo[j], hi[j]) : make_int2((int)(width + 1), -1);
+        flush(lpairs + tile_slot0, tile_slots);
+    }
+    auto stage_side = [&](bool use_hi, bool only_d, uint32_t pos) {
+#pragma unroll
+        for (int j = 0; j < kItems; ++j) {
+            if (!((vmask >> j) & 1) || (only_d && !((dmask >> j) & 1))) continue;
+            const int32_t major = (int32_t)((long long)(slot0 + j) + 1 + map.major_off);
+            stage[pos++] = make_int2(major, (int32_t)((use_hi ? hi[j] : lo[j]) + map.minor_off));
+        }
+    };
+    if (lower) {
+        stage_side(false, false, vl);
+        flush(lower + V0, tileV);
+    }
+    if (upper) {
+        stage_side(true, false, vl);
+        flush(upper + V0, tileV);
+    }
+    if (upperd) {
+        stage_side(true, true, cl - vl);
+        flush(upperd + (C0 - V0), tileC - tileV);
+    }
+    const uint32_t C = (uint32_t)pre + (uint32_t)mine, V = (uint32_t)(pre >> 32) + (uint32_t)(mine >> 32);
     if (occ) {
         // kLanesPerWord lanes x kItems slots = one 64-bit word (the first
         // slot of lane kLanesPerWord*k is 64-aligned).
@@ -251,6 +307,8 @@ extern "C" int chp_compact(chp_ctx* ctx, const int32_t* d_L, int64_t width, int6
     if (!ctx) return CHP_EINVAL;
     if (width < 1 || width > (1ll << 29)) return chp_einval(ctx, "compact: width must be in [1, 2^29]");
     if (!d_counts) return chp_einval(ctx, "compact: counts buffer required");
+    const bool big = (uint64_t)width > kSmallTileMax;
+    const uint32_t kTile = kCT * (big ? 16 : 4);
     const uint32_t ntiles = (uint32_t)((width + kTile - 1) / kTile);
     // Two status arrays of (cap + 2) words, used alternately; each launch
     // clears the other one's first ntiles entries (no memset per call).
@@ -268,14 +326,23 @@ extern "C" int chp_compact(chp_ctx* ctx, const int32_t* d_L, int64_t width, int6
     unsigned long long* st_next = base + (size_t)(cur ^ 1) * (ctx->status_cap + 2);
     if (ctx->status_clean[cur] < ntiles)
         CHP_CUDA(ctx, cudaMemsetAsync(st_cur, 0, ((size_t)ctx->status_cap + 2) * 8, ctx->stream));
+    auto kfn = big ? k_compact<16> : k_compact<4>;
     if (ctx->compact_resident == 0) {
-        int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_compact, kCT, 0);
-        ctx->compact_resident = (uint32_t)std::max(per_sm, 1) * (uint32_t)ctx->sm_count;
+        int per_sm = 0, per_sm_big = 0;  // (per-SM limits of the two forms)
+        cudaFuncSetAttribute(k_compact<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kCT * 16 * 8);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_compact<4>, kCT, 2 * kCT * 4 * 8);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_big, k_compact<16>, kCT, 2 * kCT * 16 * 8);
+        ctx->compact_resident = (uint32_t)std::max(std::min(per_sm, per_sm_big), 1) * (uint32_t)ctx->sm_count;
     }
     const int use_ticket = ntiles > ctx->compact_resident ? 1 : 0;
     Map m{major_off, minor_off, swapped};
-    CHP_CUDA(ctx, launch_pdl(k_compact, dim3(ntiles), dim3(kCT), 0, ctx->stream, (const int*)d_L, (uint32_t)width, m,
+    const size_t stage_bytes = 2 * (size_t)kTile * sizeof(int2);
+    if (big && !ctx->compact_big_attr) {
+        CHP_CUDA(ctx, cudaFuncSetAttribute(k_compact<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)stage_bytes));
+        ctx->compact_big_attr = 1;
+    }
+    CHP_CUDA(ctx, launch_pdl(kfn, dim3(ntiles), dim3(kCT), stage_bytes, ctx->stream, (const int*)d_L, (uint32_t)width, m,
                              reinterpret_cast<int2*>(d_chain), reinterpret_cast<unsigned long long*>(d_occ),
                              reinterpret_cast<int2*>(d_Lpairs), reinterpret_cast<int2*>(d_lower),
                              reinterpret_cast<int2*>(d_upper), reinterpret_cast<int2*>(d_upperd),

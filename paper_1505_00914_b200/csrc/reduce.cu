@@ -33,6 +33,7 @@
 // In sampled/filter the validation is folded into the miss path (DESIGN.md
 // §3); smem16 checks each point branch-free (two compares, a select).
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "chp_internal.cuh"
@@ -1389,12 +1390,24 @@ int run_group_filter(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, const Geo& g
     const uint64_t warm = n < (1ull << 22) ? n : (n >> kw) & ~1ull;
     chp_trace(ctx, "filter:warm");
     if ((rc = pass(d_xy, warm, nullptr))) return rc;
+    // (experiments: CHP_FILTER_YOUNG="num/den:until_shift" -- phases grow by
+    // num/den until n >> until_shift, by 2 after)
+    uint64_t y_num = 2, y_den = 1, y_until = 0;
+    if (const char* e = getenv("CHP_FILTER_YOUNG")) {
+        unsigned a = 2, b = 1, sh = 2;
+        if (sscanf(e, "%u/%u:%u", &a, &b, &sh) == 3 && a > b && b > 0) {
+            y_num = a;
+            y_den = b;
+            y_until = n >> sh;
+        }
+    }
     for (uint64_t done = warm; done < n;) {
         chp_trace(ctx, "filter:build");
         k_filter_build<W><<<(ngroups + 1 + 255) / 256, 256, 0, ctx->stream>>>(d_L, w, gshift, (int32_t)g.ybase,
                                                                             ys, (W*)ctx->filter.p, ngroups, qs);
         CHP_LAUNCHED(ctx);
-        const uint64_t stop = std::min<uint64_t>(n, 2 * done);
+        const uint64_t stop =
+            std::min<uint64_t>(n, done < y_until ? (done * y_num / y_den + 1) & ~1ull : 2 * done);
         cur_done = done;
         chp_trace(ctx, "filter:phase");
         if ((rc = pass(d_xy + 2 * done, stop - done, (const W*)ctx->filter.p))) return rc;

@@ -357,3 +357,17 @@ print("ok")
         r = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env}, capture_output=True, text=True,
                            timeout=600)
         assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("p", [(1 << 17) - 3, 1 << 17, (1 << 17) + 1, (1 << 17) + 2053, 3_000_001])
+def test_compact_tile_forms(ctx, orc, p):
+    """K3 takes 512-slot tiles up to 2^17 slots and 2048-slot tiles beyond;
+    widths around the switch, ragged last tiles and sparse columns."""
+    rng = np.random.default_rng(p)
+    n = 400_000
+    x = rng.integers(1, p + 1, size=n)
+    x[:1000] = p  # the last slot
+    x[1000:2000] = 1
+    xy = np.stack([x, rng.integers(1, 1 << 20, size=n)], axis=1).astype(np.int32)
+    got = run_device(ctx, xy, p, 1 << 20)
+    check_against_oracle(orc, got, xy, p, 1 << 20)

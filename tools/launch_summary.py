@@ -62,7 +62,7 @@ def main():
     with open(os.path.join(ROOT, "profiles", f"{rnd}_launches_config{config}.json"), "w") as f:
         json.dump(summary, f, indent=1)
     with open(os.path.join(ROOT, "profiles", f"k1_traffic_config{config}.json"), "w") as f:
-        json.dump({"config": config, "dram_bytes_per_launch": k1_bytes,
+        json.dump({"config": config, "round": rnd, "dram_bytes_per_launch": k1_bytes,
                    "what": "sum of dram__bytes_read+write over the launches of one chp_reduce call, "
                            f"from profiles/{rnd}_launches_config{config}.json"}, f, indent=1)
     print(json.dumps(summary)[:400])
