@@ -106,6 +106,8 @@ uint64_t chp_dl_len(int64_t width);
 #define CHP_REDUCE_SAMPLE_SPLIT (1u << 25) /* tuning: sampled filter's sample pass and merge as separate launches */
 #define CHP_REDUCE_BLOCKED (1u << 26) /* tuning: smem/filter streams in per-CTA contiguous slices (the sampled main pass always is) */
 #define CHP_REDUCE_SAMPLE_PREFIX (1u << 27) /* tuning: sampled filter samples the first n/2^k points (default: the head of each CTA slice) */
+#define CHP_REDUCE_WARP_AGG (1u << 28) /* global variant: warp-aggregated updates (__match_any_sync + __reduce_min_sync,
+                                          one read-compare-RED per distinct slot per warp) */
 
 /* Algorithm 1 over n int32 (x,y) pairs at d_xy (8-byte aligned).  Slot of a
  * point is x - x_off - 1; a point is valid when that slot is in [0,width)

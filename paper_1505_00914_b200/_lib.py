@@ -25,6 +25,7 @@ REDUCE_FUSED = 16384
 REDUCE_SAMPLE_SPLIT = 1 << 25
 REDUCE_BLOCKED = 1 << 26
 REDUCE_SAMPLE_PREFIX = 1 << 27
+REDUCE_WARP_AGG = 1 << 28
 
 _lib = None
 

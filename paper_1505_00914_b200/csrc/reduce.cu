@@ -453,6 +453,53 @@ __global__ void __launch_bounds__(kThreads) k_reduce_global(const int32_t* __res
     flag_error(bad, DL, width);
 }
 
+// --------------------------------------------------- global, warp-aggregated
+// north_star (a)'s form for large p or skewed columns: the lanes of a warp
+// that hold the same slot elect one leader (__match_any_sync), which applies
+// the group's min y and min ~y (__reduce_min_sync) with one read-compare-RED
+// -- one L2 round trip per distinct slot per warp instead of per point.
+// Invalid points share the match key 0xFFFFFFFF and are only flagged.
+template <bool VALIDATE>
+__global__ void __launch_bounds__(kThreads) k_reduce_global_agg(const int32_t* __restrict__ xy, uint64_t n, Geo g,
+                                                                uint32_t width, int* __restrict__ DL) {
+    const int2* gL = reinterpret_cast<const int2*>(DL);
+    const uint32_t lane = threadIdx.x & 31;
+    bool bad = false;
+    // Every lane of the warp runs the same number of rounds (a lane past the
+    // end contributes an invalid key that is not flagged).
+    auto round = [&](bool live, int32_t x, int32_t y) {
+        uint32_t s;
+        const bool ok = live && accept<VALIDATE>(g, x, y, s);
+        bad |= live && !ok;
+        const uint32_t key = ok ? s : 0xFFFFFFFFu;
+        const uint32_t grp = __match_any_sync(0xFFFFFFFFu, key);
+        const int lo = (int)__reduce_min_sync(grp, (uint32_t)(y ^ INT_MIN)) ^ INT_MIN;  // signed min
+        const int nhi = (int)__reduce_min_sync(grp, (uint32_t)(~y ^ INT_MIN)) ^ INT_MIN;
+        if (ok && lane == (uint32_t)(__ffs(grp) - 1)) {
+            const int2 e = ld_cg2(gL + s);
+            if (lo < e.x) red_min(DL + 2ull * s, lo);
+            if (nhi < e.y) red_min(DL + 2ull * s + 1, nhi);
+        }
+    };
+    const Split sp = split_points(xy, n);
+    const int4* __restrict__ v = reinterpret_cast<const int4*>(xy + 2 * sp.head);
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) - lane;
+    for (uint64_t w = warp0; w < sp.nvec; w += stride) {
+        const uint64_t i = w + lane;
+        const bool live = i < sp.nvec;
+        const int4 a = live ? ld_stream(v + i) : make_int4(0, 0, 0, 0);
+        round(live, a.x, a.y);
+        round(live, a.z, a.w);
+    }
+    if (blockIdx.x == 0 && threadIdx.x < 32) {  // the scalar head / tail points, by warp 0
+        const bool h = sp.head && lane == 0, t = sp.tail && lane == 1;
+        const int32_t* q = h ? xy : t ? xy + 2 * (n - 1) : xy;
+        round(h || t, q[0], q[1]);
+    }
+    flag_error(bad, DL, width);
+}
+
 // ------------------------------------------------------------ filter
 // Filter word per group of 2^gshift columns, two H-bit halves (H = 8 in a
 // 16-bit word, or 16 in a 32-bit word): low half fa, high half span with
@@ -1499,6 +1546,14 @@ int chp_reduce_yr(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t width, 
 
     auto launch_global = [&](const int32_t* p, uint64_t m) -> int {
         if (m == 0) return CHP_OK;
+        if (flags & CHP_REDUCE_WARP_AGG) {
+            auto fn = validate ? k_reduce_global_agg<true> : k_reduce_global_agg<false>;
+            int blocks = 0;
+            if (int rc0 = kernel_blocks(ctx, (const void*)fn, 0, 2, &blocks)) return rc0;
+            fn<<<blocks, kThreads, 0, ctx->stream>>>(p, m, g, w, d_L);
+            CHP_LAUNCHED(ctx);
+            return CHP_OK;
+        }
         const Plan pl = plan_for(ctx, 0, flags, false);
         if (validate)
             CHP_LAUNCH_PLANNED(ctx, pl, (k_reduce_global<true, true>), (k_reduce_global<true, false>), p, m, g, w,
@@ -1686,7 +1741,7 @@ int chp_reduce_yr(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t width, 
         default: {
             int rc = launch_global(d_xy, n);
             if (rc) return rc;
-            ctx->variant = "global";
+            ctx->variant = (flags & CHP_REDUCE_WARP_AGG) ? "global-agg" : "global";
             return CHP_OK;
         }
     }

@@ -21,6 +21,7 @@ pytestmark = pytest.mark.gpu
 VARIANTS = {
     "auto": 0,
     "global": _lib.REDUCE_FORCE_GLOBAL,
+    "global_agg": _lib.REDUCE_FORCE_GLOBAL | _lib.REDUCE_WARP_AGG,
     "smem32": _lib.REDUCE_FORCE_SMEM32,
     "filter": _lib.REDUCE_FORCE_FILTER,
     "filter8": _lib.REDUCE_FORCE_FILTER8,
