@@ -8,6 +8,8 @@ compares the device-reduced hull with the reference's brute-force oracle on
 10,000 mixed sets; criterion 2 the device Melkman with the reference's three
 other hulls on 1,000 sets of up to 1e5 points."""
 import os
+import re
+import statistics
 import subprocess
 
 import pytest
@@ -21,10 +23,11 @@ BIN = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), 
 @pytest.mark.skipif(not os.path.exists(BIN), reason="built only where /root/reference is present")
 def test_reference_acceptance_suite_on_dropin():
     # Criterion 8 is a wall-clock measurement (R^2 >= 0.95 of the minimum of
-    # 40 timings per n against n, n = 1e5..1e6, i.e. 0.2-0.8 ms calls): host
-    # thread wake-ups on a shared box can bend it, so a run whose ONLY failure
-    # is criterion 8 is repeated (up to three runs); every other criterion must
-    # pass in every run.
+    # 40 timings per n against n, n = 1e5..1e6, i.e. 0.2-0.8 ms calls), so one
+    # run can be bent by host scheduling on a shared box.  The suite runs three
+    # times; every other criterion must pass in every run, and criterion 8's
+    # R^2 (logged for every run) must reach 0.95 in the median of the three.
+    r2s = []
     for attempt in range(3):
         r = subprocess.run([BIN], capture_output=True, text=True, timeout=900)
         out = r.stdout + r.stderr
@@ -32,7 +35,8 @@ def test_reference_acceptance_suite_on_dropin():
             assert f"criterion {k} (" in out, out
         fails = [ln for ln in out.splitlines() if "FAIL" in ln]
         assert all("criterion 8 (" in ln for ln in fails), out
-        if not fails:
-            assert r.returncode == 0 and "all criteria passed" in out, out
-            return
-    raise AssertionError("criterion 8 failed in three runs:\n" + out)
+        m = re.search(r"criterion 8 \(.*?R\^2=([0-9.]+)", out)
+        assert m, out
+        r2s.append(float(m.group(1)))
+        print(f"run {attempt}: criterion 8 R^2 = {r2s[-1]:.4f}" + (" (FAIL)" if fails else ""))
+    assert statistics.median(r2s) >= 0.95, f"criterion 8 R^2 per run: {r2s}"
