@@ -34,7 +34,7 @@ struct chp_ctx {
     // scratch owned by the context
     DevBuf tile_status;  // K3 look-back status words: two arrays, used alternately
     uint32_t status_cap = 0, status_clean[2] = {0, 0}, compact_resident = 0;
-    int compact_big_attr = 0;
+    int compact_form = 0;  // K3 tile shape the resident count was taken for
     int status_parity = 0;
     DevBuf hull_a, hull_b, hull_cnt_a, hull_cnt_b;
     DevBuf filter;       // K1 filter snapshot

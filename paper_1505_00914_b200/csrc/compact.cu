@@ -6,25 +6,44 @@
 // (src/reducer.cpp:42-49) and serialize's (width+1,-1) form (:121-130).
 //
 // One pass over the 8-byte slots with a single-pass decoupled look-back scan
-// (tiles of 128 threads x 4 or 16 slots, tile order such that every
+// (tiles of 256 threads x 4 or 16 slots, striped; tile order such that every
 // predecessor of a tile has started).  The scanned value packs two counters
 // in a u64: c = 1 + [hi != lo] per valid slot (chain positions, Lemma-1
 // order) in the low word and v = [valid] (lower/upper positions) in the high
 // word.  Status words carry a 2-bit flag and both counters in 31 bits each,
-// hence width <= 2^29.  A warp of 8-slot masks is folded into 64-bit
-// occupancy words with three shuffles (the paper's bit array M, in
-// BlockedBitset<uint64_t> layout).
+// hence width <= 2^29.  The occupancy words (the paper's bit array M, in
+// BlockedBitset<uint64_t> layout) are warp ballots: two warps' 32 slots per
+// 64-bit word.
 #include <algorithm>
+#include <cstdlib>
 
 #include "chp_internal.cuh"
 
+// Instrumentation build only (CHP_NVCC_EXTRA=-DCHP_K3_TIMING=1): thread 0 of
+// every tile stamps %globaltimer at the phase boundaries (chp_debug_k3_phase).
+#ifndef CHP_K3_TIMING
+#define CHP_K3_TIMING 0
+#endif
+#if CHP_K3_TIMING
+__device__ unsigned long long g_k3_phase[4096][6];
+#define K3_MARK(tile, k)                                                              \
+    do {                                                                              \
+        if (threadIdx.x == 0 && (tile) < 4096) {                                     \
+            unsigned long long t_;                                                    \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                   \
+            g_k3_phase[(tile)][(k)] = t_;                                             \
+        }                                                                             \
+    } while (0)
+#else
+#define K3_MARK(tile, k) \
+    do {                 \
+    } while (0)
+#endif
+
 namespace {
 
-// 128 threads x ITEMS slots per tile.  ITEMS = 4 (512-slot tiles) up to
-// 2^17 slots, so p = 65536 spreads over 128 CTAs (2048-slot tiles left 32
-// CTAs latency-bound: 10.5 us at C2); ITEMS = 16 (2048-slot tiles) beyond,
-// so the look-back chain of p = 2^20 is 512 tiles long instead of 2048.
-constexpr int kCT = 128;  // threads per tile
+// Tiles of 256 threads x 4 slots up to 2^17 slots (p = 65536: 64 CTAs),
+// 256 x 16 beyond (p = 2^20: 256 CTAs, so the look-back chain is short).
 constexpr uint32_t kSmallTileMax = 1u << 17;
 
 constexpr unsigned long long kFlagAgg = 1ull << 62;
@@ -59,7 +78,77 @@ __device__ __forceinline__ int2 to_original(const Map& m, long long slot1, long 
     return m.swapped ? make_int2(minor, major) : make_int2(major, minor);
 }
 
-template <int kItems>
+// Decoupled look-back by warp 0 of a tile: publishes the tile's aggregate,
+// returns the exclusive prefix of all preceding tiles (every lane), and
+// publishes the inclusive value.  Looks back over a window of 256
+// predecessors at once (8 per lane, all loads in flight together): every tile
+// publishes its aggregate right after its local scan, so one window usually
+// settles the prefix in a single L2 round trip instead of a chain of 32-tile
+// steps.  Indices below 0 read as an inclusive zero.
+__device__ __forceinline__ unsigned long long lookback(unsigned long long* __restrict__ status, uint32_t tile,
+                                                       unsigned long long tile_agg, int lane) {
+    unsigned long long excl = 0;
+    if (tile == 0) {
+        if (lane == 0) st_release(status + tile, pack_status(kFlagIncl, tile_agg));
+        return 0;
+    }
+    if (lane == 0) st_release(status + tile, pack_status(kFlagAgg, tile_agg));
+    constexpr int kPer = 8;
+    long long top = (long long)tile - 1;
+    for (;;) {
+        unsigned long long st[kPer];
+        long long idx[kPer];
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            idx[k] = top - lane - 32 * k;
+            st[k] = idx[k] >= 0 ? ld_acquire(status + idx[k]) : kFlagIncl;
+        }
+        // Re-poll every not-yet-published predecessor together, one round
+        // trip per pass (a per-slot spin serialised up to 8 L2 round trips
+        // per lane: the look-back took ~6 us at C2).
+        for (;;) {
+            uint32_t pending = 0;
+#pragma unroll
+            for (int k = 0; k < kPer; ++k) pending |= (uint32_t)((st[k] >> 62) == 0) << k;
+            if (!__any_sync(0xffffffffu, pending != 0)) break;
+#pragma unroll
+            for (int k = 0; k < kPer; ++k)
+                if ((pending >> k) & 1) st[k] = ld_acquire(status + idx[k]);
+        }
+        long long best = LLONG_MIN;  // nearest inclusive predecessor in the window
+#pragma unroll
+        for (int k = 0; k < kPer; ++k)
+            if ((st[k] >> 62) == 2 && idx[k] > best) best = idx[k];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const long long b = __shfl_xor_sync(0xffffffffu, best, o);
+            best = b > best ? b : best;
+        }
+        unsigned long long val = 0;
+#pragma unroll
+        for (int k = 0; k < kPer; ++k)
+            if (idx[k] >= best && idx[k] >= 0) val += unpack_cv(st[k]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+        excl += val;
+        if (best != LLONG_MIN) break;
+        top -= 32 * kPer;
+    }
+    if (lane == 0) st_release(status + tile, pack_status(kFlagIncl, excl + tile_agg));
+    return excl;
+}
+
+// One tile = kCT threads x kItems slots, STRIPED: item j of thread t is slot
+// tile_slot0 + j * kCT + t, so every load of L, and every store of each
+// output, is a warp-contiguous run (a blocked layout -- each thread owning
+// kItems consecutive slots -- needed a shared-memory stage whose scattered
+// writes were 32-way bank conflicts: 8 us of a 20 us call at p = 2^20).
+// Chain positions follow slot order, i.e. (item, warp, lane) order: a warp
+// scan per item, the (item, warp) totals prefix-summed once in shared memory,
+// then the tile's look-back prefix.  Counters per value: c = 1 + [hi != lo]
+// (chain) in bits 0-15 and v = [valid] in bits 16-31 (tile-local sums stay
+// below 2^16).
+template <int kCT, int kItems>
 __global__ void __launch_bounds__(kCT) k_compact(const int* __restrict__ DL, uint32_t width, Map map,
                                                  int2* __restrict__ chain, unsigned long long* __restrict__ occ,
                                                  int2* __restrict__ lpairs, int2* __restrict__ lower,
@@ -68,11 +157,13 @@ __global__ void __launch_bounds__(kCT) k_compact(const int* __restrict__ DL, uin
                                                  unsigned long long* __restrict__ status,
                                                  unsigned long long* __restrict__ status_next, uint32_t ntiles,
                                                  int use_ticket) {
-    constexpr int kLanesPerWord = 64 / kItems;
+    static_assert(kCT % 64 == 0, "a warp pair must cover whole 64-bit occupancy words");
+    constexpr int kWarps = kCT / 32;
     constexpr int kTile = kCT * kItems;
+    static_assert(2 * kTile < 65536, "tile-local counters are 16-bit");
     __shared__ uint32_t s_tile;
-    __shared__ unsigned long long s_warp[kCT / 32];
-    __shared__ unsigned long long s_excl;
+    __shared__ uint32_t s_tot[kItems * kWarps];  // per (item, warp): c | v << 16, then its exclusive prefix
+    __shared__ unsigned long long s_excl, s_agg;
     pdl_wait();  // DL from K1 (launched as a programmatic dependent)
     // Tile order: block index when every tile's CTA is co-resident (no
     // predecessor can be waiting for a slot), else an atomic ticket so that
@@ -84,6 +175,7 @@ __global__ void __launch_bounds__(kCT) k_compact(const int* __restrict__ DL, uin
         __syncthreads();
         tile = s_tile;
     }
+    K3_MARK(tile, 0);
     // The next call uses the other status array: clear it here instead of a
     // cudaMemset before every launch.
     if (threadIdx.x == 0) {
@@ -91,202 +183,103 @@ __global__ void __launch_bounds__(kCT) k_compact(const int* __restrict__ DL, uin
         if (tile == 0) reinterpret_cast<unsigned int*>(status_next + ntiles)[0] = 0u;
     }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint64_t slot0 = (uint64_t)tile * kTile + (uint64_t)threadIdx.x * kItems;
+    const uint64_t tile_slot0 = (uint64_t)tile * kTile;
     const int2* gL = reinterpret_cast<const int2*>(DL);
 
     int lo[kItems], hi[kItems];
-    uint32_t vmask = 0, dmask = 0;
-    if (slot0 + kItems <= width && !(reinterpret_cast<uintptr_t>(DL) & 15)) {
-        // whole thread in range: 16-byte loads, all in flight together
-        const int4* g4 = reinterpret_cast<const int4*>(gL + slot0);
-        int4 q[kItems / 2];
 #pragma unroll
-        for (int j = 0; j < kItems / 2; ++j) q[j] = g4[j];  // (L1: the lane's later loads hit its sectors)
-#pragma unroll
-        for (int j = 0; j < kItems / 2; ++j) {
-            lo[2 * j] = q[j].x;
-            hi[2 * j] = ~q[j].y;
-            lo[2 * j + 1] = q[j].z;
-            hi[2 * j + 1] = ~q[j].w;
-        }
-    } else {
-#pragma unroll
-        for (int j = 0; j < kItems; ++j) {
-            const uint64_t s = slot0 + j;
-            lo[j] = CHP_EMPTY;
-            hi[j] = INT_MIN;
-            if (s < width) {
-                const int2 e = gL[s];
-                lo[j] = e.x;
-                hi[j] = ~e.y;
-            }
-        }
+    for (int j = 0; j < kItems; ++j) {  // all loads in flight together
+        const uint64_t s = tile_slot0 + (uint64_t)j * kCT + threadIdx.x;
+        int2 e = make_int2(CHP_EMPTY, CHP_EMPTY);
+        if (s < width) e = __ldcg(gL + s);
+        lo[j] = e.x;
+        hi[j] = ~e.y;
     }
+    uint32_t ex[kItems];  // lane-exclusive (c | v << 16) within the warp, per item
 #pragma unroll
     for (int j = 0; j < kItems; ++j) {
-        if (lo[j] <= hi[j]) {
-            vmask |= 1u << j;
-            if (lo[j] != hi[j]) dmask |= 1u << j;
-        }
-    }
-    const uint32_t nv = __popc(vmask), nd = __popc(dmask);
-    const unsigned long long mine = (unsigned long long)(nv + nd) | ((unsigned long long)nv << 32);
-
-    // Block exclusive scan of `mine`.
-    unsigned long long incl = mine;
+        const bool v = lo[j] <= hi[j];
+        const uint32_t mine = v ? (lo[j] != hi[j] ? 2u : 1u) | (1u << 16) : 0u;
+        uint32_t incl = mine;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += t;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        ex[j] = incl - mine;
+        if (lane == 31) s_tot[j * kWarps + warp] = incl;
     }
-    if (lane == 31) s_warp[warp] = incl;
     __syncthreads();
     if (warp == 0) {
-        unsigned long long w = lane < kCT / 32 ? s_warp[lane] : 0ull;
+        // exclusive prefix over the kItems * kWarps (item, warp) totals, in order
+        constexpr int kN = kItems * kWarps;
+        constexpr int kPerLane = (kN + 31) / 32;
+        uint32_t t[kPerLane], sum = 0;
 #pragma unroll
-        for (int o = 1; o < kCT / 32; o <<= 1) {
-            const unsigned long long t = __shfl_up_sync(0xffffffffu, w, o);
-            if (lane >= o) w += t;
+        for (int k = 0; k < kPerLane; ++k) {
+            const int i = lane * kPerLane + k;
+            t[k] = i < kN ? s_tot[i] : 0u;
+            sum += t[k];
         }
-        if (lane < kCT / 32) s_warp[lane] = w;  // inclusive warp prefix
+        uint32_t incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += u;
+        }
+        uint32_t run = incl - sum;
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < kPerLane; ++k) {
+            const int i = lane * kPerLane + k;
+            if (i < kN) s_tot[i] = run;
+            run += t[k];
+        }
+        K3_MARK(tile, 1);
+        const unsigned long long agg = (unsigned long long)(total & 0xFFFFu) | ((unsigned long long)(total >> 16) << 32);
+        const unsigned long long excl = lookback(status, tile, agg, lane);
+        if (lane == 0) {
+            s_excl = excl;
+            s_agg = agg;
+        }
     }
     __syncthreads();
-    const unsigned long long warp_excl = warp ? s_warp[warp - 1] : 0ull;
-    const unsigned long long tile_agg = s_warp[kCT / 32 - 1];
-    const unsigned long long thread_excl = warp_excl + incl - mine;
-
-    // Decoupled look-back (warp 0).
-    if (warp == 0) {
-        unsigned long long excl = 0;
-        if (tile == 0) {
-            if (lane == 0) st_release(status + tile, pack_status(kFlagIncl, tile_agg));
-        } else {
-            if (lane == 0) st_release(status + tile, pack_status(kFlagAgg, tile_agg));
-            // Look back over a window of 256 predecessors at once (8 per
-            // lane, all loads in flight together): every tile publishes its
-            // aggregate right after its local scan, so one window usually
-            // settles the prefix in a single L2 round trip instead of a
-            // chain of 32-tile steps.  Indices below 0 read as an
-            // inclusive zero.
-            constexpr int kPer = 8;
-            long long top = (long long)tile - 1;
-            for (;;) {
-                unsigned long long st[kPer];
-                long long idx[kPer];
-#pragma unroll
-                for (int k = 0; k < kPer; ++k) {
-                    idx[k] = top - lane - 32 * k;
-                    st[k] = idx[k] >= 0 ? ld_acquire(status + idx[k]) : kFlagIncl;
-                }
-                // Re-poll every not-yet-published predecessor together, one
-                // round trip per pass (a per-slot spin serialised up to 8
-                // L2 round trips per lane: the look-back took ~6 us at C2).
-                for (;;) {
-                    uint32_t pending = 0;
-#pragma unroll
-                    for (int k = 0; k < kPer; ++k) pending |= (uint32_t)((st[k] >> 62) == 0) << k;
-                    if (!__any_sync(0xffffffffu, pending != 0)) break;
-#pragma unroll
-                    for (int k = 0; k < kPer; ++k)
-                        if ((pending >> k) & 1) st[k] = ld_acquire(status + idx[k]);
-                }
-                long long best = LLONG_MIN;  // nearest inclusive predecessor in the window
-#pragma unroll
-                for (int k = 0; k < kPer; ++k)
-                    if ((st[k] >> 62) == 2 && idx[k] > best) best = idx[k];
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    const long long b = __shfl_xor_sync(0xffffffffu, best, o);
-                    best = b > best ? b : best;
-                }
-                unsigned long long val = 0;
-#pragma unroll
-                for (int k = 0; k < kPer; ++k)
-                    if (idx[k] >= best && idx[k] >= 0) val += unpack_cv(st[k]);
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
-                excl += val;
-                if (best != LLONG_MIN) break;
-                top -= 32 * kPer;
-            }
-            if (lane == 0) st_release(status + tile, pack_status(kFlagIncl, excl + tile_agg));
-        }
-        if (lane == 0) s_excl = excl;
-    }
-    __syncthreads();
+    K3_MARK(tile, 2);
     const unsigned long long tile_pre = s_excl;
-    const unsigned long long pre = tile_pre + thread_excl;
-    const uint32_t C0 = (uint32_t)tile_pre, V0 = (uint32_t)(tile_pre >> 32);  // the tile's first positions
-    const uint32_t tileC = (uint32_t)tile_agg, tileV = (uint32_t)(tile_agg >> 32);
-    const uint64_t tile_slot0 = (uint64_t)tile * kTile;
-    const uint32_t tile_slots = (uint32_t)(width - tile_slot0 < (uint64_t)kTile ? width - tile_slot0 : kTile);
-
-    // Outputs go through a shared-memory stage, one output at a time, and
-    // leave the tile as contiguous runs: written straight from registers,
-    // each warp store touched 32 sectors for 8 bytes apiece (ncu, C4: 2.1 M
-    // store sectors for 16 MB of chain, 31 sectors per request).
-    extern __shared__ int2 stage[];  // 2 * kTile points
-    auto flush = [&](int2* __restrict__ dst, uint32_t count) {
-        __syncthreads();
-        for (uint32_t k = threadIdx.x; k < count; k += kCT) dst[k] = stage[k];
-        __syncthreads();
-    };
-    const uint32_t cl = (uint32_t)thread_excl, vl = (uint32_t)(thread_excl >> 32);  // local positions
-    if (chain) {
-        uint32_t c = cl;
+    const uint32_t C0 = (uint32_t)tile_pre, V0 = (uint32_t)(tile_pre >> 32);
 #pragma unroll
-        for (int j = 0; j < kItems; ++j) {
-            if (!((vmask >> j) & 1)) continue;
-            const long long slot1 = (long long)(slot0 + j) + 1;
-            stage[c] = to_original(map, slot1, lo[j]);
-            if ((dmask >> j) & 1) stage[c + 1] = to_original(map, slot1, hi[j]);
-            c += ((dmask >> j) & 1) ? 2 : 1;
+    for (int j = 0; j < kItems; ++j) {
+        const uint64_t s = tile_slot0 + (uint64_t)j * kCT + threadIdx.x;
+        const bool v = lo[j] <= hi[j], d = v && lo[j] != hi[j];
+        const uint32_t pre = s_tot[j * kWarps + warp] + ex[j];
+        const uint32_t C = C0 + (pre & 0xFFFFu), V = V0 + (pre >> 16);
+        if (lpairs && s < width) lpairs[s] = v ? make_int2(lo[j], hi[j]) : make_int2((int)(width + 1), -1);
+        if (occ) {
+            // warps 2k and 2k+1 of an item cover one 64-slot word: its halves
+            const uint32_t bits = __ballot_sync(0xffffffffu, v);
+            const uint64_t s0 = tile_slot0 + (uint64_t)j * kCT + (uint64_t)warp * 32;
+            if (lane == 0 && (s0 >> 6) < ((uint64_t)width + 63) / 64)  // (the word exists)
+                reinterpret_cast<uint32_t*>(occ)[s0 >> 5] = bits;
         }
-        flush(chain + C0, tileC);
-    }
-    if (lpairs) {
-#pragma unroll
-        for (int j = 0; j < kItems; ++j)
-            stage[threadIdx.x * kItems + j] =
-                ((vmask >> j) & 1) ? make_int2(lo[j], hi[j]) : make_int2((int)(width + 1), -1);
-        flush(lpairs + tile_slot0, tile_slots);
-    }
-    auto stage_side = [&](bool use_hi, bool only_d, uint32_t pos) {
-#pragma unroll
-        for (int j = 0; j < kItems; ++j) {
-            if (!((vmask >> j) & 1) || (only_d && !((dmask >> j) & 1))) continue;
-            const int32_t major = (int32_t)((long long)(slot0 + j) + 1 + map.major_off);
-            stage[pos++] = make_int2(major, (int32_t)((use_hi ? hi[j] : lo[j]) + map.minor_off));
+        if (!v) continue;
+        const long long slot1 = (long long)s + 1;
+        if (chain) {
+            chain[C] = to_original(map, slot1, lo[j]);
+            if (d) chain[C + 1] = to_original(map, slot1, hi[j]);
         }
-    };
-    if (lower) {
-        stage_side(false, false, vl);
-        flush(lower + V0, tileV);
+        const int32_t major = (int32_t)(slot1 + map.major_off);
+        if (lower) lower[V] = make_int2(major, (int32_t)(lo[j] + map.minor_off));
+        if (upper) upper[V] = make_int2(major, (int32_t)(hi[j] + map.minor_off));
+        if (upperd && d) upperd[C - V] = make_int2(major, (int32_t)(hi[j] + map.minor_off));
     }
-    if (upper) {
-        stage_side(true, false, vl);
-        flush(upper + V0, tileV);
-    }
-    if (upperd) {
-        stage_side(true, true, cl - vl);
-        flush(upperd + (C0 - V0), tileC - tileV);
-    }
-    const uint32_t C = (uint32_t)pre + (uint32_t)mine, V = (uint32_t)(pre >> 32) + (uint32_t)(mine >> 32);
-    if (occ) {
-        // kLanesPerWord lanes x kItems slots = one 64-bit word (the first
-        // slot of lane kLanesPerWord*k is 64-aligned).
-        unsigned long long word = (unsigned long long)vmask << (kItems * (lane % kLanesPerWord));
-#pragma unroll
-        for (int o = 1; o < kLanesPerWord; o <<= 1) word |= __shfl_xor_sync(0xffffffffu, word, o);
-        const uint64_t wi = slot0 >> 6;
-        if (lane % kLanesPerWord == 0 && wi * 64 < width) occ[wi] = word;
-    }
-    if (tile == ntiles - 1 && threadIdx.x == kCT - 1) {
-        // The last tile's last thread holds the totals.
-        counts[0] = (long long)C;
-        counts[1] = (long long)V;
+    K3_MARK(tile, 3);
+    if (tile == ntiles - 1 && threadIdx.x == 0) {
+        const unsigned long long tot = tile_pre + s_agg;
+        counts[0] = (long long)(uint32_t)tot;
+        counts[1] = (long long)(uint32_t)(tot >> 32);
         counts[2] = (long long)DL[2ull * width];
-        counts[3] = (long long)(C - V);
+        counts[3] = (long long)((uint32_t)tot - (uint32_t)(tot >> 32));
     }
 }
 
@@ -308,7 +301,19 @@ extern "C" int chp_compact(chp_ctx* ctx, const int32_t* d_L, int64_t width, int6
     if (width < 1 || width > (1ll << 29)) return chp_einval(ctx, "compact: width must be in [1, 2^29]");
     if (!d_counts) return chp_einval(ctx, "compact: counts buffer required");
     const bool big = (uint64_t)width > kSmallTileMax;
-    const uint32_t kTile = kCT * (big ? 16 : 4);
+    // Tile shape (threads x slots per thread): 256 x 4 up to 2^17 slots,
+    // 256 x 16 beyond (CHP_K3_SMALL / CHP_K3_BIG pick others, experiments).
+    // Measured alone (tools/k3_bench.py) -- C2, p = 2^16: 128x4 3.5, 256x4 3.3,
+    // 256x2 3.7, 128x8 3.8, 64x8 4.2 us; C4, p = 2^20: 256x16 9.3, 128x16
+    // 13.6, 256x8 14.1, 512x4 13.9, 128x8 15.0 us.
+    static const int small_form = getenv("CHP_K3_SMALL") ? atoi(getenv("CHP_K3_SMALL")) : 5;
+    static const int big_form = getenv("CHP_K3_BIG") ? atoi(getenv("CHP_K3_BIG")) : 1;
+    static const int forms[][2] = {{128, 4}, {256, 16}, {256, 8}, {512, 4}, {128, 8}, {256, 4}, {64, 8}, {256, 2},
+                                   {128, 16}};
+    const int f = big ? big_form : small_form;
+    const int fi = f >= 0 && f < 9 ? f : 0;
+    int thr = forms[fi][0], items = forms[fi][1];
+    const uint32_t kTile = (uint32_t)(thr * items);
     const uint32_t ntiles = (uint32_t)((width + kTile - 1) / kTile);
     // Two status arrays of (cap + 2) words, used alternately; each launch
     // clears the other one's first ntiles entries (no memset per call).
@@ -326,23 +331,24 @@ extern "C" int chp_compact(chp_ctx* ctx, const int32_t* d_L, int64_t width, int6
     unsigned long long* st_next = base + (size_t)(cur ^ 1) * (ctx->status_cap + 2);
     if (ctx->status_clean[cur] < ntiles)
         CHP_CUDA(ctx, cudaMemsetAsync(st_cur, 0, ((size_t)ctx->status_cap + 2) * 8, ctx->stream));
-    auto kfn = big ? k_compact<16> : k_compact<4>;
-    if (ctx->compact_resident == 0) {
-        int per_sm = 0, per_sm_big = 0;  // (per-SM limits of the two forms)
-        cudaFuncSetAttribute(k_compact<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kCT * 16 * 8);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_compact<4>, kCT, 2 * kCT * 4 * 8);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_big, k_compact<16>, kCT, 2 * kCT * 16 * 8);
-        ctx->compact_resident = (uint32_t)std::max(std::min(per_sm, per_sm_big), 1) * (uint32_t)ctx->sm_count;
+    decltype(&k_compact<128, 4>) kfn = k_compact<128, 4>;
+    if (thr == 256 && items == 16) kfn = k_compact<256, 16>;
+    if (thr == 256 && items == 8) kfn = k_compact<256, 8>;
+    if (thr == 512 && items == 4) kfn = k_compact<512, 4>;
+    if (thr == 128 && items == 8) kfn = k_compact<128, 8>;
+    if (thr == 256 && items == 4) kfn = k_compact<256, 4>;
+    if (thr == 64 && items == 8) kfn = k_compact<64, 8>;
+    if (thr == 256 && items == 2) kfn = k_compact<256, 2>;
+    if (thr == 128 && items == 16) kfn = k_compact<128, 16>;
+    if (ctx->compact_resident == 0 || ctx->compact_form != thr * 64 + items) {
+        int per_sm = 0;
+        CHP_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)kfn, thr, 0));
+        ctx->compact_resident = (uint32_t)std::max(per_sm, 1) * (uint32_t)ctx->sm_count;
+        ctx->compact_form = thr * 64 + items;
     }
     const int use_ticket = ntiles > ctx->compact_resident ? 1 : 0;
     Map m{major_off, minor_off, swapped};
-    const size_t stage_bytes = 2 * (size_t)kTile * sizeof(int2);
-    if (big && !ctx->compact_big_attr) {
-        CHP_CUDA(ctx, cudaFuncSetAttribute(k_compact<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)stage_bytes));
-        ctx->compact_big_attr = 1;
-    }
-    CHP_CUDA(ctx, launch_pdl(kfn, dim3(ntiles), dim3(kCT), stage_bytes, ctx->stream, (const int*)d_L, (uint32_t)width, m,
+    CHP_CUDA(ctx, launch_pdl(kfn, dim3(ntiles), dim3(thr), 0, ctx->stream, (const int*)d_L, (uint32_t)width, m,
                              reinterpret_cast<int2*>(d_chain), reinterpret_cast<unsigned long long*>(d_occ),
                              reinterpret_cast<int2*>(d_Lpairs), reinterpret_cast<int2*>(d_lower),
                              reinterpret_cast<int2*>(d_upper), reinterpret_cast<int2*>(d_upperd),
@@ -353,6 +359,12 @@ extern "C" int chp_compact(chp_ctx* ctx, const int32_t* d_L, int64_t width, int6
     ctx->status_parity = cur ^ 1;
     return CHP_OK;
 }
+
+#if CHP_K3_TIMING
+extern "C" int chp_debug_k3_phase(unsigned long long* out) {
+    return (int)cudaMemcpyFromSymbol(out, g_k3_phase, sizeof(g_k3_phase));
+}
+#endif
 
 extern "C" int chp_ns_chain(chp_ctx* ctx, const int32_t* d_lower, const int32_t* d_upperd,
                             const int64_t* d_counts, int64_t width, int32_t* d_ns) {

@@ -362,8 +362,9 @@ print("ok")
 
 @pytest.mark.parametrize("p", [(1 << 17) - 3, 1 << 17, (1 << 17) + 1, (1 << 17) + 2053, 3_000_001])
 def test_compact_tile_forms(ctx, orc, p):
-    """K3 takes 512-slot tiles up to 2^17 slots and 2048-slot tiles beyond;
-    widths around the switch, ragged last tiles and sparse columns."""
+    """K3 takes 1024-slot tiles (256 threads x 4, striped) up to 2^17 slots
+    and 4096-slot tiles (256 x 16) beyond; widths around the switch, ragged
+    last tiles, partial occupancy words and sparse columns."""
     rng = np.random.default_rng(p)
     n = 400_000
     x = rng.integers(1, p + 1, size=n)
