@@ -359,3 +359,29 @@ def test_precondition_speculative_window8(ctx, orc, pinned):
     assert out["bbox"] == ref["bbox"]
     assert np.array_equal(out["chain"], ref["chain"])
     assert np.array_equal(out["hull"], ref["hull"])
+
+
+# The two halves of chp_pipeline_host (chp_reduce_host, chp_finish_host):
+# partial DLs from separate host slices, merged by an element-wise MIN, give
+# the one-call result; the error word survives the merge.
+@pytest.mark.parametrize("config,p", [(2, 65536), (4, 1 << 20), (5, 256)])
+@pytest.mark.parametrize("pinned", [False, True])
+def test_reduce_host_finish_host_halves(ctx, orc, config, p, pinned):
+    n = 20_000_003
+    xy = generate_host(config, config, p, n)
+    if pinned:
+        xy = _pinned(xy)
+    cut = 7_777_777
+    a = ctx.reduce_host(xy[:cut], p, p)
+    b = ctx.reduce_host(xy[cut:], p, p)
+    merged = torch.minimum(a, b)
+    out = ctx.finish_host(merged, p, L=True, chain=True, hull=True)
+    ref = orc.pipeline(xy, p, p)
+    assert np.array_equal(out["L"], ref["L"])
+    assert out["s"] == ref["s"] and np.array_equal(out["chain"], ref["chain"])
+    assert np.array_equal(out["hull"], ref["hull"])
+    bad = np.array(xy[cut:cut + 1000])
+    bad[500] = (p + 1, 1)
+    c = ctx.reduce_host(bad, p, p)  # no raise here: the error word stays in the DL
+    with pytest.raises(ValueError):
+        ctx.finish_host(torch.minimum(a, c), p)
