@@ -42,7 +42,7 @@ struct chp_ctx {
     DevBuf gridbar;      // grid barrier of the cooperative sampled kernel
     DevBuf yrange;       // K1 sampled filter, q unset: per-CTA y range of a prefix
     int coop = 0;        // cudaDevAttrCooperativeLaunch
-    int hull_coop_checked = 0, hull_coop_ok = 0, hull_leaf_attr = 0;  // K4 launch shape (hull.cu)
+    int hull_coop_checked = 0, hull_coop_ok = 0, hull_leaf_attr = 0, hull_small_attr = 0;  // K4 launch shape (hull.cu)
     DevBuf dl;           // host pipeline: device-form L
     DevBuf counts;       // host pipeline: int64[8]
     DevBuf chain, lower, upper, hull, occ, lpairs;

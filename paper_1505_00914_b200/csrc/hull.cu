@@ -236,6 +236,7 @@ __device__ __forceinline__ void final_block(const P* __restrict__ fin, const int
 constexpr int kLeafThreads = 128;  // leaf threads per CTA: stacks of 128 x 32 x 16 B = 64 KB
 constexpr size_t kLeafSmem = (size_t)kLeafThreads * kLeaf * sizeof(P);
 constexpr int kCoopThreads = 512;
+constexpr uint32_t kSmallChunks = 64;  // one-CTA form up to 64 chunks per problem
 static_assert((kCoopThreads / 32) * kStage * sizeof(P) <= kLeafSmem, "merge slabs reuse the leaf stacks");
 
 __global__ void __launch_bounds__(kLeafThreads) k_hull_leaf(const int2* __restrict__ lower,
@@ -281,7 +282,8 @@ __global__ void __launch_bounds__(kCoopThreads, 1)
                        buf0, cnt0);
         }
     }
-    grid_barrier(bar);
+    // (a single CTA -- small widths, launched plainly -- needs no grid barrier)
+    if (gridDim.x == 1) __syncthreads(); else grid_barrier(bar);
     P *bin = buf0, *bout = buf1;
     int *cin = cnt0, *cout = cnt1;
     uint32_t nregions = nchunks;
@@ -293,7 +295,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1)
         for (uint32_t gw = gw0; gw < 2 * npairs; gw += warps)
             merge_pair(gw, threadIdx.x & 31, bin, cin, bout, cout, nchunks, cap, nregions, region_cap,
                        stacks + (threadIdx.x >> 5) * kStage);  // the leaf stacks, free after the leaves
-        grid_barrier(bar);
+        if (gridDim.x == 1) __syncthreads(); else grid_barrier(bar);
         P* tb = bin;
         bin = bout;
         bout = tb;
@@ -303,7 +305,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1)
         nregions = npairs;
         region_cap *= 2;
     }
-    grid_barrier_done(bar);
+    if (gridDim.x > 1) grid_barrier_done(bar);
     if (blockIdx.x == 0) final_block(bin, cin, nchunks, cap, counts, swapped, tmp, hull, h_out);
 }
 
@@ -328,6 +330,22 @@ extern "C" int chp_hull(chp_ctx* ctx, const int32_t* d_lower, const int32_t* d_u
     // CHP_HULL_LAUNCHES=1 (tests): the multi-launch form even when the
     // cooperative kernel is available.
     static const bool force_launches = getenv("CHP_HULL_LAUNCHES") != nullptr;
+    // Small widths (<= 64 chunks a problem, 2048 columns): the same kernel as
+    // ONE CTA, block barriers instead of grid barriers, a plain launch (C5,
+    // p = 256: one CTA of 512 threads instead of 148 behind 3 grid barriers).
+    if (nchunks <= kSmallChunks && !force_launches) {
+        if (!ctx->hull_small_attr) {
+            CHP_CUDA(ctx, cudaFuncSetAttribute(k_hull_coop, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)kLeafSmem));
+            ctx->hull_small_attr = 1;
+        }
+        k_hull_coop<<<1, kCoopThreads, kLeafSmem, ctx->stream>>>(
+            reinterpret_cast<const int2*>(d_lower), reinterpret_cast<const int2*>(d_upper), counts, nchunks, cap,
+            bufs[0], bufs[1], cnts[0], cnts[1], swapped, tmp, reinterpret_cast<int2*>(d_hull),
+            reinterpret_cast<long long*>(d_h), nullptr);
+        CHP_LAUNCHED(ctx);
+        return CHP_OK;
+    }
     if (ctx->coop && !force_launches) {
         if (!ctx->gridbar.p) {
             if ((rc = chp_ensure(ctx, ctx->gridbar, 64))) return rc;
