@@ -373,3 +373,30 @@ def test_compact_tile_forms(ctx, orc, p):
     xy = np.stack([x, rng.integers(1, 1 << 20, size=n)], axis=1).astype(np.int32)
     got = run_device(ctx, xy, p, 1 << 20)
     check_against_oracle(orc, got, xy, p, 1 << 20)
+
+
+def test_maximum_width(ctx, orc):
+    """The device limit, width = 2^29 columns (31-bit look-back counters;
+    SURVEY.md 8(b)): a sparse input over the whole width, the first and last
+    slot included, through K1 (group filter), K3 and K4 against the oracle."""
+    p = 1 << 29
+    free = torch.cuda.mem_get_info()[0]
+    if free < (100 << 30) or _host_mem_available() < (48 << 30):
+        pytest.skip("needs ~100 GiB of free device memory and ~48 GiB of host RAM")
+    rng = np.random.default_rng(29)
+    n = 2_000_000
+    xy = np.stack([rng.integers(1, p + 1, size=n), rng.integers(1, 1 << 30, size=n)], axis=1).astype(np.int32)
+    xy[:5] = [[1, 7], [1, 9], [p, 3], [p, 1 << 29], [p // 2, 5]]
+    got = run_device(ctx, xy, p, None)
+    check_against_oracle(orc, got, xy, p, None)
+
+
+def test_width_beyond_device_limit_rejected(ctx):
+    """Beyond 2^29 columns the compaction and hull refuse (ValueError, the
+    drop-in's std::invalid_argument) instead of overflowing their counters."""
+    p = (1 << 29) + 1
+    DL = torch.empty(2, dtype=torch.int32, device="cuda")
+    with pytest.raises(ValueError):
+        ctx.compact(DL, p, chain=False)
+    with pytest.raises(ValueError):
+        ctx.pipeline_host(np.array([[1, 1]], np.int32), p, 5)
