@@ -13,16 +13,16 @@ invocation and are reported under `per_config` (same split, same timing).
 
 A step = one pass of the path over the batch: K1 (chp_reduce: DL init +
 Algorithm 1) on each rank's slice resident in HBM, then (N > 1) the path's
-one exchange -- an element-wise MIN all-reduce of the partial device-form L
-over NCCL -- then K3 (chp_compact: Lemma-1 chain + counts).  `value` = n /
+one exchange -- an element-wise MIN reduce of the partial device-form L onto
+rank 0 over NCCL -- then K3 (chp_compact: Lemma-1 chain + counts).  `value` = n /
 (max over ranks of the device-timed K steps / K).  The hull (K4) is timed
 separately (`hull_ms`), outside `value`, as BASELINE.json prescribes.
 
 `e2e` is the same metric through the public C-ABI call a user makes, from
 pinned HOST memory, host<->device copies inside the timed region: at N = 1
 chp_pipeline_host (chunked H2D overlapped with K1, K3, chain back); at N > 1
-each rank chp_reduce_host on its slice, the NCCL MIN all-reduce, then rank 0
-chp_finish_host (K3, chain back).
+each rank chp_reduce_host on its slice, the NCCL MIN reduce onto rank 0, then
+rank 0 chp_finish_host (K3, chain back).
 
 `--impl reference` times the reference's own CPU implementation
 (oracle/_ref/libchpref.so: chp::reducer::reduce + build_polyline compiled
@@ -281,9 +281,12 @@ class Arm:
 
     def combine(self, DL):
         if self.world > 1:
-            from paper_1505_00914_b200.shard import allreduce_dl
+            from paper_1505_00914_b200.shard import reduce_dl
 
-            allreduce_dl(DL)  # the path's one exchange: element-wise MIN of the partial Ls
+            # the path's one exchange: element-wise MIN of the partial Ls onto
+            # rank 0, whose K3 produces the chain (the other ranks compact
+            # their partial L, which nobody reads)
+            reduce_dl(DL, dst=0)
 
     def measure(self, cfg: int, n_total: int, e2e: bool) -> dict:
         torch, ctx, args, stream = self.torch, self.ctx, self.args, self.stream
@@ -457,7 +460,7 @@ class Arm:
         h2d = int(self.sum_over_ranks(float(h2d)))
         packed = h2d < n_total * 8
         path = ("chp_pipeline_host" if self.world == 1 else
-                "per rank chp_reduce_host on its slice, NCCL MIN all-reduce of L, rank 0 chp_finish_host") + \
+                "per rank chp_reduce_host on its slice, NCCL MIN reduce of L onto rank 0, rank 0 chp_finish_host") + \
                " (pinned int32 input; " + \
                (("8 Mi-point chunks packed to 2-byte slot|y points (8 bits each)" if p <= 256 else
                  "8 Mi-point chunks packed to 16-bit slot|y words" if p <= 65536 else

@@ -3,10 +3,11 @@
 Min and max are associative, commutative and exact on integers, so any
 partition of the points gives the same L.  Each rank reduces its own points
 into a device-form L (DL: pairs (lo, ~hi), empty = INT32_MAX, then the error
-word); storing ~hi makes every word a MIN, so ONE element-wise MIN
-all-reduce merges the partials -- NCCL over NVLink/NVSwitch on the GPU box
-(torch.distributed, backend "nccl"), gloo in the CPU tests.  The merged DL
-is then compacted (K3) on every rank.
+word); storing ~hi makes every word a MIN, so ONE element-wise MIN merges
+the partials -- NCCL over NVLink/NVSwitch on the GPU box (torch.distributed,
+backend "nccl"), gloo in the CPU tests: an all-reduce when every rank needs
+the merged L (allreduce_dl), a reduce onto one rank when only that rank
+compacts it (reduce_dl; bench.py, rank 0).
 
 The host helpers pack/unpack the same DL layout (tests, host-side merges).
 """
@@ -34,6 +35,22 @@ def allreduce_dl(DL, group=None):
         DL.copy_(host)
         return DL
     dist.all_reduce(DL, op=dist.ReduceOp.MIN, group=group)
+    return DL
+
+
+def reduce_dl(DL, dst: int = 0, group=None):
+    """Element-wise MIN of the partial DLs onto rank `dst` only (K3 runs
+    there; the other ranks' DL stays partial): half the traffic of the
+    all-reduce for the same merged L."""
+    import torch.distributed as dist
+
+    if DL.is_cuda and dist.get_backend(group) == "gloo":  # CPU test path
+        host = DL.cpu()
+        dist.reduce(host, dst=dst, op=dist.ReduceOp.MIN, group=group)
+        if dist.get_rank(group) == dst:
+            DL.copy_(host)
+        return DL
+    dist.reduce(DL, dst=dst, op=dist.ReduceOp.MIN, group=group)
     return DL
 
 

@@ -20,7 +20,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, xy, p, q, out):
+def _worker(rank, world, port, xy, p, q, out, op="allreduce"):
     import oracle
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -33,18 +33,23 @@ def _worker(rank, world, port, xy, p, q, out):
     ok = (part[:, 0] >= 1) & (part[:, 0] <= p) & (part[:, 1] >= 1) & ((q is None) | (part[:, 1] <= (q or 0)))
     arr = orc.reduce(part[ok], p, q)
     DL = torch.from_numpy(dl_pack_host(arr["lo"], arr["hi"], arr["valid"], err=int((~ok).any())))
-    dist.all_reduce(DL, op=dist.ReduceOp.MIN)
+    if op == "allreduce":
+        dist.all_reduce(DL, op=dist.ReduceOp.MIN)
+    else:
+        from paper_1505_00914_b200.shard import reduce_dl
+
+        reduce_dl(DL, dst=0)
     if rank == 0:
         out.put(DL.numpy().copy())
     dist.barrier()
     dist.destroy_process_group()
 
 
-def _run(xy, p, q, world=2):
+def _run(xy, p, q, world=2, op="allreduce"):
     ctx = mp.get_context("spawn")
     out = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, xy, p, q, out)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, xy, p, q, out, op)) for r in range(world)]
     for pr in procs:
         pr.start()
     DL = out.get(timeout=120)
@@ -91,3 +96,17 @@ def test_two_rank_error_word_propagates(orc):
     xy = np.array([[1, 1], [2, 2], [3, 3], [9, 1]], np.int32)  # x=9 > p=5 on rank 1's shard
     DL = _run(xy, 5, 5)
     assert dl_unpack_host(DL)[3] == -1
+
+
+def test_two_rank_min_reduce_onto_rank0(orc):
+    """bench.py's combine: the MIN reduce onto rank 0 (shard.reduce_dl)."""
+    from paper_1505_00914_b200.device import generate_host
+
+    p = 65536
+    xy = generate_host(2, 2, p, 300_000)
+    DL = _run(xy, p, p, op="reduce")
+    lo, hi, valid, err = dl_unpack_host(DL)
+    arr = orc.reduce(xy, p, p)
+    assert err == 0
+    L = np.stack([np.where(valid, lo, p + 1), np.where(valid, hi, -1)], axis=1)
+    assert np.array_equal(L, orc.L_pairs(arr))
