@@ -16,7 +16,11 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
-LIB = os.path.join(LIBDIR, "libchp_b200.so")
+# CHP_LIB_VARIANT (diagnostics): a separately built library, e.g. "bounds"
+# (CHP_NVCC_EXTRA=-DCHP_BOUNDS=1: device-side index checks that trap) as
+# lib/libchp_b200_bounds.so, loaded instead of the product library.
+_VARIANT = os.environ.get("CHP_LIB_VARIANT", "")
+LIB = os.path.join(LIBDIR, "libchp_b200%s.so" % (("_" + _VARIANT) if _VARIANT else ""))
 INCLUDE = os.path.join(ROOT, "include")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -51,7 +55,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
-    objdir = os.path.join(ROOT, "build", "obj")
+    objdir = os.path.join(ROOT, "build", "obj" + (("_" + _VARIANT) if _VARIANT else ""))
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <climits>
+#include <cstdio>
 #include <cstdint>
 #include <cstdio>
 #include <string>
@@ -141,6 +142,20 @@ int chp_reduce_yr(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t width, 
                   int64_t x_off, int32_t* d_L, uint32_t flags);
 
 // ----------------------------------------------------------- device side
+
+// Diagnostics build (CHP_NVCC_EXTRA=-DCHP_BOUNDS=1, CHP_LIB_VARIANT=bounds):
+// index checks on the output writes of the kernels that trap on failure --
+// compute-sanitizer is not available on the test pool.
+#ifndef CHP_BOUNDS
+#define CHP_BOUNDS 0
+#endif
+#define CHP_CHECK(cond)                                                              \
+    do {                                                                             \
+        if (CHP_BOUNDS && !(cond)) {                                                 \
+            printf("chp bounds check failed: %s (%s:%d)\n", #cond, __FILE__, __LINE__); \
+            __trap();                                                                \
+        }                                                                            \
+    } while (0)
 
 // 128-bit streaming load: read-only path, no L1 allocation, 256-byte L2
 // sector prefetch (the point stream is touched exactly once, sequentially).

@@ -254,11 +254,15 @@ __global__ void __launch_bounds__(kCT) k_compact(const int* __restrict__ DL, uin
         const bool v = lo[j] <= hi[j], d = v && lo[j] != hi[j];
         const uint32_t pre = s_tot[j * kWarps + warp] + ex[j];
         const uint32_t C = C0 + (pre & 0xFFFFu), V = V0 + (pre >> 16);
+        CHP_CHECK(!v || s < width);
+        CHP_CHECK(!v || C + (d ? 1u : 0u) < 2u * width);
+        CHP_CHECK(!v || V < width);
         if (lpairs && s < width) lpairs[s] = v ? make_int2(lo[j], hi[j]) : make_int2((int)(width + 1), -1);
         if (occ) {
             // warps 2k and 2k+1 of an item cover one 64-slot word: its halves
             const uint32_t bits = __ballot_sync(0xffffffffu, v);
             const uint64_t s0 = tile_slot0 + (uint64_t)j * kCT + (uint64_t)warp * 32;
+            CHP_CHECK((s0 & 31) == 0);
             if (lane == 0 && (s0 >> 6) < ((uint64_t)width + 63) / 64)  // (the word exists)
                 reinterpret_cast<uint32_t*>(occ)[s0 >> 5] = bits;
         }
@@ -276,6 +280,7 @@ __global__ void __launch_bounds__(kCT) k_compact(const int* __restrict__ DL, uin
     K3_MARK(tile, 3);
     if (tile == ntiles - 1 && threadIdx.x == 0) {
         const unsigned long long tot = tile_pre + s_agg;
+        CHP_CHECK((uint32_t)tot <= 2u * width && (uint32_t)(tot >> 32) <= width);
         counts[0] = (long long)(uint32_t)tot;
         counts[1] = (long long)(uint32_t)(tot >> 32);
         counts[2] = (long long)DL[2ull * width];

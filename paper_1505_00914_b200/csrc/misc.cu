@@ -191,8 +191,10 @@ __global__ void k_unpack8(const uint4* __restrict__ in8, uint64_t n, int32_t bas
     }
     if (blockIdx.x == 0) {
         const uint16_t* in16 = reinterpret_cast<const uint16_t*>(in8);
-        for (uint64_t j = 8 * nw + threadIdx.x; j < n; j += blockDim.x)
+        for (uint64_t j = 8 * nw + threadIdx.x; j < n; j += blockDim.x) {
+            CHP_CHECK(j < n && j / 8 == nw);
             out[j] = make_int2((int)(in16[j] & 0xFFu) + base, (int)(in16[j] >> 8) + ybase);
+        }
     }
 }
 }  // namespace

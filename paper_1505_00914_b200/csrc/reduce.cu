@@ -243,6 +243,8 @@ template <bool READ_FIRST, int N>
 __device__ __forceinline__ void settle_misses(uint32_t miss, const uint32_t (&s)[N], const int (&y)[N],
                                               int* __restrict__ DL) {
     if (!miss) return;
+#pragma unroll
+    for (int k = 0; k < N; ++k) CHP_CHECK(!((miss >> k) & 1) || s[k] < 0x7FFFFFFFu);
     const int2* gL = reinterpret_cast<const int2*>(DL);
     if (READ_FIRST) {
         int2 e[N];
@@ -1043,6 +1045,7 @@ __device__ __forceinline__ void sampled_pass(const int32_t* __restrict__ xy, uin
             bad = 1;
             return;
         }
+        CHP_CHECK(s < width);
         const uint32_t a = tbase + 2 * s;
         const uint32_t w = lds_u16(a);
         const uint32_t lo = w & 0xFFu, span = w >> 8;
