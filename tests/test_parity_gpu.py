@@ -247,7 +247,7 @@ def test_full_size_vs_oracle(ctx, orc, config):
     """BASELINE.json configs 3-5 at full size (1e9 / 1e9 / 4e9 points)
     against the oracle, bit for bit: L (serialize form), occupancy words,
     s, the Lemma-1 chain, the north_star chain and the hull, for the auto
-    variant and every forced K1 variant.  The oracle reads the device's own
+    variant (q given and q unset) and every forced K1 variant.  The oracle reads the device's own
     input bytes back in 1 GB chunks and reduces them with SURVEY.md 8(c)'s
     chunked procedure (reduce per slice on host threads, slot-by-slot merge,
     then the survivors reduced once more), so nothing of 8-32 GB has to sit
@@ -263,8 +263,11 @@ def test_full_size_vs_oracle(ctx, orc, config):
         pytest.skip(f"needs {(n * 8 + (1 << 30)) / 2**30:.1f} GiB of free device memory")
     d = ctx.generate(config, seed, p, n)
     got = {}
-    for name in FULL_VARIANTS:
-        DL = ctx.reduce(d, p, q=p, flags=VARIANTS[name])
+    for name in FULL_VARIANTS + ("auto_q_unset",):
+        # (q unset: the reference API's default; every y is valid here, so the
+        # L is the same and the speculative-range variants must reproduce it)
+        q = None if name == "auto_q_unset" else p
+        DL = ctx.reduce(d, p, q=q, flags=VARIANTS.get(name, 0))
         comp = ctx.compact(DL, p, chain=True, occ=True, lpairs=True, lower=True, upper=True, upperd=True)
         hull = ctx.hull(comp, p)
         ns = ctx.ns_chain(comp, p)
