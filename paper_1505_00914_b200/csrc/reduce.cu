@@ -538,6 +538,8 @@ template <typename W>
 __global__ void __launch_bounds__(256) k_filter_build(const int* __restrict__ DL, uint32_t width, uint32_t gshift,
                                                       int32_t ybase, uint32_t ys, W* __restrict__ F,
                                                       uint32_t ngroups, const int2* __restrict__ qs) {
+    pdl_trigger();  // the next phase may queue (its CTAs wait for this grid)
+    pdl_wait();     // the previous phase's updates of DL
     const uint32_t gi = blockIdx.x * blockDim.x + threadIdx.x;
     if (gi > ngroups) return;
     if (qs) {  // q unset: the speculative bucket range (k_quant_shift)
@@ -612,6 +614,11 @@ __global__ void __launch_bounds__((READ_FIRST && !TMA) ? kThreadsRF : kThreads) 
     W* sF = reinterpret_cast<W*>(sF4);
     const uint32_t nwords = ngroups + 1;
     uint8_t* ring = reinterpret_cast<uint8_t*>(sF4) + table_span((size_t)nwords * sizeof(W));
+    // Launched as a programmatic dependent of the snapshot build (or of the
+    // DL init): the next build may queue at once, and this grid waits for
+    // its predecessor's table (and DL) before reading them.
+    pdl_trigger();
+    pdl_wait();
     {
         const uint32_t per4 = 16 / sizeof(W);
         const uint32_t n4 = nwords / per4;
@@ -1415,17 +1422,18 @@ int run_group_filter(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, const Geo& g
             CHP_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
             int per_sm = 0;
             CHP_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreadsRF, pl.smem));
-            fn<<<std::max(1, std::min(per_sm, 2)) * ctx->sm_count, kThreadsRF, pl.smem, ctx->stream>>>(
-                xy, cnt, g, w, gshift, ys, F, ngroups, pl.stages, d_L, qs);
+            CHP_CUDA(ctx, launch_pdl(fn, dim3(std::max(1, std::min(per_sm, 2)) * ctx->sm_count), dim3(kThreadsRF),
+                                     pl.smem, ctx->stream, xy, cnt, g, w, gshift, ys, F, ngroups, pl.stages, d_L,
+                                     qs));
             CHP_LAUNCHED(ctx);
         } else if (rf)
-            CHP_LAUNCH_PLANNED(ctx, pl, (k_reduce_filter<W, true, true, SPEC>), (k_reduce_filter<W, true, false, SPEC>),
-                               xy, cnt,
-                               g, w, gshift, ys, F, ngroups, pl.stages, d_L, qs);
+            CHP_LAUNCH_PLANNED_PDL(ctx, pl, (k_reduce_filter<W, true, true, SPEC>),
+                                   (k_reduce_filter<W, true, false, SPEC>), xy, cnt, g, w, gshift, ys, F, ngroups,
+                                   pl.stages, d_L, qs);
         else
-            CHP_LAUNCH_PLANNED(ctx, pl, (k_reduce_filter<W, false, true, SPEC>),
-                               (k_reduce_filter<W, false, false, SPEC>), xy,
-                               cnt, g, w, gshift, ys, F, ngroups, pl.stages, d_L, qs);
+            CHP_LAUNCH_PLANNED_PDL(ctx, pl, (k_reduce_filter<W, false, true, SPEC>),
+                                   (k_reduce_filter<W, false, false, SPEC>), xy, cnt, g, w, gshift, ys, F, ngroups,
+                                   pl.stages, d_L, qs);
         return CHP_OK;
     };
     // Phases double in length: warm-up n/2^kw (default n/64) with an empty
@@ -1442,22 +1450,34 @@ int run_group_filter(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, const Geo& g
     if ((rc = pass(d_xy, warm, nullptr))) return rc;
     // (experiments: CHP_FILTER_YOUNG="num/den:until_shift" -- phases grow by
     // num/den until n >> until_shift, by 2 after)
-    uint64_t y_num = 2, y_den = 1, y_until = 0;
-    if (const char* e = getenv("CHP_FILTER_YOUNG")) {
-        unsigned a = 2, b = 1, sh = 2;
-        if (sscanf(e, "%u/%u:%u", &a, &b, &sh) == 3 && a > b && b > 0) {
-            y_num = a;
-            y_den = b;
-            y_until = n >> sh;
+    // (CHP_FILTER_SPLIT_LAST: the last phase in two halves with a rebuild
+    // between, to measure what one phase boundary costs)
+    struct Young {
+        unsigned num = 2, den = 1, shift = 64;
+        bool split_last = false;
+    };
+    static const Young young = [] {
+        Young y;
+        if (const char* e = getenv("CHP_FILTER_YOUNG")) {
+            unsigned a = 2, b = 1, sh = 2;
+            if (sscanf(e, "%u/%u:%u", &a, &b, &sh) == 3 && a > b && b > 0) {
+                y.num = a;
+                y.den = b;
+                y.shift = sh;
+            }
         }
-    }
+        y.split_last = getenv("CHP_FILTER_SPLIT_LAST") != nullptr;
+        return y;
+    }();
+    const uint64_t y_num = young.num, y_den = young.den, y_until = young.shift >= 64 ? 0 : n >> young.shift;
     for (uint64_t done = warm; done < n;) {
         chp_trace(ctx, "filter:build");
-        k_filter_build<W><<<(ngroups + 1 + 255) / 256, 256, 0, ctx->stream>>>(d_L, w, gshift, (int32_t)g.ybase,
-                                                                            ys, (W*)ctx->filter.p, ngroups, qs);
+        CHP_CUDA(ctx, launch_pdl(k_filter_build<W>, dim3((ngroups + 1 + 255) / 256), dim3(256), 0, ctx->stream,
+                                 (const int*)d_L, w, gshift, (int32_t)g.ybase, ys, (W*)ctx->filter.p, ngroups, qs));
         CHP_LAUNCHED(ctx);
-        const uint64_t stop =
-            std::min<uint64_t>(n, done < y_until ? (done * y_num / y_den + 1) & ~1ull : 2 * done);
+        uint64_t stop = std::min<uint64_t>(n, done < y_until ? (done * y_num / y_den + 1) & ~1ull : 2 * done);
+        if (young.split_last && stop == n && done >= n / 2 && n - done > (n >> 3))
+            stop = (done + (n - done) / 2) & ~1ull;
         cur_done = done;
         chp_trace(ctx, "filter:phase");
         if ((rc = pass(d_xy + 2 * done, stop - done, (const W*)ctx->filter.p))) return rc;
