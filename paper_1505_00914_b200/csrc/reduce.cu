@@ -314,6 +314,7 @@ __host__ __device__ constexpr size_t table_span(size_t table_bytes) { return (ta
 
 // ------------------------------------------------------------- DL init
 __global__ void k_dl_init(int4* __restrict__ DL4, uint64_t nwords4, int* __restrict__ DL, uint32_t width) {
+    pdl_trigger();  // K1 may queue; it waits for this grid before touching DL
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nwords4; i += stride)
         DL4[i] = make_int4(CHP_EMPTY, CHP_EMPTY, CHP_EMPTY, CHP_EMPTY);
@@ -346,6 +347,7 @@ __global__ void __launch_bounds__(kThreads) k_reduce_smem32(const int32_t* __res
         if (~y < e.y) atomicMin(&sL[s].y, ~y);
     };
     stream_points<TMA>(xy, n, ring, stages, per_point4(f), f);
+    pdl_wait();  // (a programmatic dependent of the DL init: only the flush touches DL)
     flag_error(bad, DL, width);
     __syncthreads();
     // Flush: only slots where this CTA beats the current global value.
@@ -402,6 +404,12 @@ __global__ void __launch_bounds__(kThreads) k_reduce_smem16(const int32_t* __res
         }
     };
     stream_points<TMA>(xy, n, ring, stages, per_point4(one), one, g.blocked != 0);
+    // A programmatic dependent of the DL init: the stream above does not
+    // touch DL, so only the flush waits for it.  (Streaming the points
+    // before the wait is valid because no kernel that writes points -- the
+    // generators, unpack, translate -- triggers its dependents early; the
+    // kernels that do write only DL, tables and snapshots.)
+    pdl_wait();
     flag_error(bad != 0, DL, width);
     __syncthreads();
     int2* __restrict__ gL = reinterpret_cast<int2*>(DL);
@@ -1591,10 +1599,10 @@ int chp_reduce_yr(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t width, 
         case V_SMEM32: {
             const Plan pl = plan_for(ctx, (size_t)w * 8, flags, true);
             if (validate)
-                CHP_LAUNCH_PLANNED(ctx, pl, (k_reduce_smem32<true, true>), (k_reduce_smem32<true, false>), d_xy, n,
+                CHP_LAUNCH_PLANNED_PDL(ctx, pl, (k_reduce_smem32<true, true>), (k_reduce_smem32<true, false>), d_xy, n,
                                    g, w, pl.stages, d_L);
             else
-                CHP_LAUNCH_PLANNED(ctx, pl, (k_reduce_smem32<false, true>), (k_reduce_smem32<false, false>), d_xy,
+                CHP_LAUNCH_PLANNED_PDL(ctx, pl, (k_reduce_smem32<false, true>), (k_reduce_smem32<false, false>), d_xy,
                                    n, g, w, pl.stages, d_L);
             ctx->variant = pl.tma ? "smem32+tma" : "smem32";
             return CHP_OK;
@@ -1603,7 +1611,7 @@ int chp_reduce_yr(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t width, 
             const Plan pl = plan_for(ctx, (size_t)w * 4, flags, false);
             // fits16 implies validation with 1 <= y <= q <= 65536 (the kernel's
             // packed window).
-            CHP_LAUNCH_PLANNED(ctx, pl, k_reduce_smem16<true>, k_reduce_smem16<false>, d_xy, n, g, w, pl.stages,
+            CHP_LAUNCH_PLANNED_PDL(ctx, pl, k_reduce_smem16<true>, k_reduce_smem16<false>, d_xy, n, g, w, pl.stages,
                                d_L);
             ctx->variant = pl.tma ? "smem16+tma" : "smem16";
             return CHP_OK;
