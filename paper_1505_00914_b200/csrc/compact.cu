@@ -165,6 +165,9 @@ __global__ void __launch_bounds__(kCT) k_compact(const int* __restrict__ DL, uin
     __shared__ uint32_t s_tot[kItems * kWarps];  // per (item, warp): c | v << 16, then its exclusive prefix
     __shared__ unsigned long long s_excl, s_agg;
     pdl_wait();  // DL from K1 (launched as a programmatic dependent)
+    // (No early trigger here: a caller may reduce K3's own chain next, and
+    // the kernels that stream points before their wait rely on their
+    // immediate predecessor never writing points.)
     // Tile order: block index when every tile's CTA is co-resident (no
     // predecessor can be waiting for a slot), else an atomic ticket so that
     // a tile only starts after all its predecessors have.

@@ -314,7 +314,11 @@ __host__ __device__ constexpr size_t table_span(size_t table_bytes) { return (ta
 
 // ------------------------------------------------------------- DL init
 __global__ void k_dl_init(int4* __restrict__ DL4, uint64_t nwords4, int* __restrict__ DL, uint32_t width) {
-    pdl_trigger();  // K1 may queue; it waits for this grid before touching DL
+    // A programmatic dependent itself (the previous call's K3 reads DL), and
+    // the trigger comes after the wait: K1, which streams its points before
+    // waiting, may then overlap this grid only, never a kernel before it.
+    pdl_wait();
+    pdl_trigger();
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nwords4; i += stride)
         DL4[i] = make_int4(CHP_EMPTY, CHP_EMPTY, CHP_EMPTY, CHP_EMPTY);
@@ -405,10 +409,11 @@ __global__ void __launch_bounds__(kThreads) k_reduce_smem16(const int32_t* __res
     };
     stream_points<TMA>(xy, n, ring, stages, per_point4(one), one, g.blocked != 0);
     // A programmatic dependent of the DL init: the stream above does not
-    // touch DL, so only the flush waits for it.  (Streaming the points
-    // before the wait is valid because no kernel that writes points -- the
-    // generators, unpack, translate -- triggers its dependents early; the
-    // kernels that do write only DL, tables and snapshots.)
+    // touch DL, so only the flush waits for it.  Streaming the points before
+    // the wait is valid because it can overlap only the immediate
+    // predecessor, and no kernel that triggers its dependents early writes
+    // points (they write DL, tables and snapshots; K3, the generators,
+    // unpack and translate do not trigger early).
     pdl_wait();
     flag_error(bad != 0, DL, width);
     __syncthreads();
@@ -852,7 +857,7 @@ __global__ void k_quant_shift(const int2* __restrict__ part, uint32_t np, Geo g,
 // Phase helpers shared by the three-launch pipeline and the fused kernel.
 __device__ __forceinline__ void sample_init(uint4* smem4, uint32_t wpad, int* __restrict__ DL, uint32_t width,
                                             int init_dl) {
-    for (uint32_t c = threadIdx.x; c < wpad / 8; c += blockDim.x)  // ua = 255 > ub = 0: empty
+    for (uint32_t c = threadIdx.x; smem4 && c < wpad / 8; c += blockDim.x)  // ua = 255 > ub = 0: empty
         smem4[c] = make_uint4(0x00FF00FFu, 0x00FF00FFu, 0x00FF00FFu, 0x00FF00FFu);
     if (init_dl) {
         const uint64_t words = 2ull * width;
@@ -1182,11 +1187,16 @@ __global__ void __launch_bounds__(kThreads) k_sampled_fused(const int32_t* __res
     if (merge_only) pdl_trigger();  // the main pass (a dependent launch) may queue
     phase_mark(0);
     if (SPEC) qz = resolve_quant(qz, qpart, nqpart, g);
-    // ---- A: sample pass + DL init
-    sample_init(smem4, wpad, DL, width, init_dl);
+    // ---- A: sample pass, then DL init.  Launched as a programmatic
+    // dependent (when the runtime allows it with a cooperative launch), the
+    // fold of the points runs before waiting for the predecessor (the
+    // previous call's K3, which reads DL); only the DL init waits.
+    sample_init(smem4, wpad, DL, width, 0);
     __syncthreads();
     phase_mark(1);
     sample_fold<false, SPEC>(xy, n, f256, prefix != 0, g, width, qz, reinterpret_cast<uint16_t*>(smem4), nullptr, 0);
+    pdl_wait();
+    if (init_dl) sample_init(nullptr, 0, DL, width, 1);
     __syncthreads();
     phase_mark(2);
     sample_dump(smem4, scratch, wpad);
@@ -1506,7 +1516,8 @@ extern "C" int chp_dl_init(chp_ctx* ctx, int32_t* d_L, int64_t width) {
     const bool aligned = (reinterpret_cast<uintptr_t>(d_L) & 15) == 0;
     const uint64_t n4 = aligned ? words / 4 : 0;
     const int blocks = (int)std::min<uint64_t>((n4 + 255) / 256 + 1, (uint64_t)ctx->sm_count * 8);
-    k_dl_init<<<blocks, 256, 0, ctx->stream>>>(reinterpret_cast<int4*>(d_L), n4, d_L, (uint32_t)width);
+    CHP_CUDA(ctx, launch_pdl(k_dl_init, dim3(blocks), dim3(256), 0, ctx->stream, reinterpret_cast<int4*>(d_L), n4, d_L,
+                             (uint32_t)width));
     CHP_LAUNCHED(ctx);
     return CHP_OK;
 }
@@ -1700,8 +1711,26 @@ int chp_reduce_yr(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t width, 
                     // split form below runs instead.)
                     static const bool refuse = getenv("CHP_TEST_COOP_REFUSE") != nullptr;  // tests
                     chp_trace(ctx, "sampled:sample+merge");
-                    const cudaError_t ce = cudaLaunchCooperativeKernel(fused, dim3(sblocks * (refuse ? 64 : 1)),
-                                                                       dim3(kThreads), args, smem, ctx->stream);
+                    // Cooperative AND a programmatic dependent of the
+                    // previous kernel (it waits before touching DL); plain
+                    // cooperative if the runtime refuses the pair.
+                    cudaLaunchConfig_t lc = {};
+                    lc.gridDim = dim3(sblocks * (refuse ? 64 : 1));
+                    lc.blockDim = dim3(kThreads);
+                    lc.dynamicSmemBytes = smem;
+                    lc.stream = ctx->stream;
+                    cudaLaunchAttribute la[2];
+                    la[0].id = cudaLaunchAttributeCooperative;
+                    la[0].val.cooperative = 1;
+                    la[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+                    la[1].val.programmaticStreamSerializationAllowed = 1;
+                    lc.attrs = la;
+                    lc.numAttrs = 2;
+                    cudaError_t ce = cudaLaunchKernelExC(&lc, fused, args);
+                    if (ce != cudaSuccess && !refuse) {
+                        cudaGetLastError();
+                        ce = cudaLaunchCooperativeKernel(fused, dim3(sblocks), dim3(kThreads), args, smem, ctx->stream);
+                    }
                     if (ce != cudaSuccess) {
                         cudaGetLastError();
                         goto split;

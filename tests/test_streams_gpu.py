@@ -106,3 +106,28 @@ def test_many_cooperative_launches_reuse_the_barrier(orc):
     assert np.array_equal(comp["chain"][:s].cpu().numpy(), chain)
     h = int(hull["h"].item())
     assert np.array_equal(hull["hull"][:h].cpu().numpy(), hull_ref)
+
+
+@pytest.mark.parametrize("config,p", [(2, 65536), (5, 256), (4, 1 << 20), (3, 16384)])
+def test_reduce_own_chain_right_after_compact(ctx, orc, config, p):
+    """Back-to-back calls where each consumes the previous one's output
+    (the kernels that stream points before their programmatic wait must
+    never overlap the kernel that wrote those points): reduce, compact,
+    reduce the chain K3 just wrote (no copy), compact again -- idempotence,
+    many times over without host synchronisation."""
+    xy = generate_host(config, config, p, 4_000_000)
+    d = torch.from_numpy(xy).cuda()
+    arr = orc.reduce(xy, p, p)
+    ref_chain = orc.build_polyline(arr)
+    s = len(ref_chain)
+    outs = []
+    for _ in range(20):
+        DL = ctx.reduce(d, p, q=p)
+        comp = ctx.compact(DL, p, chain=True)
+        DL2 = ctx.reduce(comp["chain"][:s], p, q=p)
+        comp2 = ctx.compact(DL2, p, chain=True)
+        outs.append(comp2)
+    torch.cuda.synchronize()
+    for comp2 in outs:
+        assert int(comp2["counts"][0].item()) == s
+        assert np.array_equal(comp2["chain"][:s].cpu().numpy(), ref_chain)
