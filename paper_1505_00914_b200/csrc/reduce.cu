@@ -1728,6 +1728,12 @@ int chp_reduce_yr(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t width, 
                     lc.numAttrs = 2;
                     cudaError_t ce = cudaLaunchKernelExC(&lc, fused, args);
                     if (ce != cudaSuccess && !refuse) {
+                        static bool told = false;
+                        if (!told && getenv("CHP_VERBOSE")) {
+                            fprintf(stderr, "chp: cooperative + programmatic launch refused (%s); cooperative only\n",
+                                    cudaGetErrorString(ce));
+                            told = true;
+                        }
                         cudaGetLastError();
                         ce = cudaLaunchCooperativeKernel(fused, dim3(sblocks), dim3(kThreads), args, smem, ctx->stream);
                     }
