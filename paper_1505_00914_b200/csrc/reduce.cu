@@ -547,19 +547,11 @@ __device__ __forceinline__ uint32_t lds_w(uint32_t addr) {
 // loads in flight (a warp-per-group form left half the lanes idle and ran
 // one round trip per wave: 16 us per snapshot at p = 2^20).  Word
 // `ngroups` (the sink) and a partial last group are "never".
-template <typename W>
-__global__ void __launch_bounds__(256) k_filter_build(const int* __restrict__ DL, uint32_t width, uint32_t gshift,
-                                                      int32_t ybase, uint32_t ys, W* __restrict__ F,
-                                                      uint32_t ngroups, const int2* __restrict__ qs) {
-    pdl_trigger();  // the next phase may queue (its CTAs wait for this grid)
-    pdl_wait();     // the previous phase's updates of DL
-    const uint32_t gi = blockIdx.x * blockDim.x + threadIdx.x;
-    if (gi > ngroups) return;
-    if (qs) {  // q unset: the speculative bucket range (k_quant_shift)
-        const int2 v = __ldcg(qs);
-        ybase = v.x;
-        ys = (uint32_t)v.y;
-    }
+// The snapshot word of group gi from DL (with the bucket base and shift);
+// kLoads 16-byte loads in flight per thread.
+template <typename W, int kLoads = 8>
+__device__ __forceinline__ W filter_word(const int* __restrict__ DL, uint32_t width, uint32_t gshift,
+                                         int32_t ybase, uint32_t ys, uint32_t gi, uint32_t ngroups) {
     const uint32_t c0 = gi << gshift;
     const uint32_t c1 = c0 + (1u << gshift);
     W word = FW<W>::kNever;
@@ -575,13 +567,13 @@ __global__ void __launch_bounds__(256) k_filter_build(const int* __restrict__ DL
         if (gshift >= 1 && !(reinterpret_cast<uintptr_t>(DL) & 15)) {  // 16-byte aligned pairs
             const int4* p4 = reinterpret_cast<const int4*>(DL) + (c0 >> 1);
             const uint32_t n4 = 1u << (gshift - 1);
-            for (uint32_t i = 0; i < n4; i += 8) {
-                int4 q[8];
+            for (uint32_t i = 0; i < n4; i += kLoads) {
+                int4 q[kLoads];
 #pragma unroll
-                for (int k = 0; k < 8; ++k)
+                for (int k = 0; k < kLoads; ++k)
                     if (i + k < n4) q[k] = __ldcg(p4 + i + k);
 #pragma unroll
-                for (int k = 0; k < 8; ++k)
+                for (int k = 0; k < kLoads; ++k)
                     if (i + k < n4) {
                         fold(q[k].x, q[k].y);
                         fold(q[k].z, q[k].w);
@@ -608,7 +600,27 @@ __global__ void __launch_bounds__(256) k_filter_build(const int* __restrict__ DL
             }
         }
     }
-    F[gi] = word;
+    return word;
+}
+
+// One thread per group, its columns read as 16-byte pairs with up to 8
+// loads in flight (a warp-per-group form left half the lanes idle and ran
+// one round trip per wave: 16 us per snapshot at p = 2^20).  Word
+// `ngroups` (the sink) and a partial last group are "never".
+template <typename W>
+__global__ void __launch_bounds__(256) k_filter_build(const int* __restrict__ DL, uint32_t width, uint32_t gshift,
+                                                      int32_t ybase, uint32_t ys, W* __restrict__ F,
+                                                      uint32_t ngroups, const int2* __restrict__ qs) {
+    pdl_trigger();  // the next phase may queue (its CTAs wait for this grid)
+    pdl_wait();     // the previous phase's updates of DL
+    const uint32_t gi = blockIdx.x * blockDim.x + threadIdx.x;
+    if (gi > ngroups) return;
+    if (qs) {  // q unset: the speculative bucket range (k_quant_shift)
+        const int2 v = __ldcg(qs);
+        ybase = v.x;
+        ys = (uint32_t)v.y;
+    }
+    F[gi] = filter_word<W>(DL, width, gshift, ybase, ys, gi, ngroups);
 }
 
 // F == nullptr starts from an all-"never skip" table (the warm-up pass:
