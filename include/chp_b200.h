@@ -273,7 +273,10 @@ uint64_t chp_group_last_h2d_bytes(const chp_group* g);
 /* Device-resident shards: d_xy[k] (n[k] points) on shard k's device.  On
  * return (asynchronous, on the shards' context streams) d_L[0] holds the
  * merged DL -- with CHP_COMBINE_NCCL every d_L[k] does.  Compact it with
- * chp_compact on chp_group_ctx(g, 0). */
+ * chp_compact on chp_group_ctx(g, 0).  Later work on any shard's stream is
+ * ordered after the combine (CHP_COMBINE_PEER: each shard stream waits for
+ * the combine kernel's reads of its partial).  The group calls leave the
+ * caller's current device unchanged. */
 int chp_reduce_sharded(chp_group* g, const int32_t* const* d_xy, const uint64_t* n, int64_t width, int64_t q,
                        int32_t* const* d_L);
 /* chp_pipeline_host over the group: one host thread per shard streams its

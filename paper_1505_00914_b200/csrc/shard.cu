@@ -94,6 +94,7 @@ struct chp_group {
     std::vector<chp_ctx*> ctx;
     std::vector<ncclComm_t> comm;
     std::vector<cudaEvent_t> folded;  // per shard: its partial DL is complete
+    cudaEvent_t combined = nullptr;   // (peer) the combine kernel has read every partial
     std::string err;
     uint64_t h2d_bytes = 0;
 };
@@ -152,13 +153,30 @@ int combine(chp_group* g, int32_t* const* d_L, int64_t width) {
     c0->launches++;
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return gfail(g, CHP_EDEVICE, std::string("k_dl_min_peers: ") + cudaGetErrorString(e));
+    // Later work on a shard's stream (the next call's DL init) must not
+    // overwrite its partial while the combine still reads it.
+    if (cudaEventRecord(g->combined, c0->stream) != cudaSuccess) return gfail(g, CHP_EDEVICE, "cudaEventRecord");
+    for (int k = 1; k < g->G; ++k) {
+        cudaSetDevice(g->dev[k]);
+        if (cudaStreamWaitEvent(g->ctx[k]->stream, g->combined, 0) != cudaSuccess)
+            return gfail(g, CHP_EDEVICE, "cudaStreamWaitEvent");
+    }
     return CHP_OK;
 }
+
+// The caller's current device, restored on exit (the group calls switch
+// between the shards' devices).
+struct DeviceGuard {
+    int dev = 0;
+    DeviceGuard() { cudaGetDevice(&dev); }
+    ~DeviceGuard() { cudaSetDevice(dev); }
+};
 
 template <typename T>
 int pipeline_sharded(chp_group* g, const T* h_xy, uint64_t n, int64_t width, int64_t q, int32_t* h_Lpairs,
                      uint64_t* h_occ, int32_t* h_chain, int64_t* h_s, int32_t* h_hull, int64_t* h_h) {
     if (!g) return CHP_EINVAL;
+    DeviceGuard keep;
     g->h2d_bytes = 0;
     if (width < 1) return gfail(g, CHP_EINVAL, "reduce: width must be >= 1");
     if (width > (1ll << 29)) return gfail(g, CHP_EINVAL, "reduce: width exceeds the device limit 2^29");
@@ -202,6 +220,7 @@ extern "C" {
 
 int chp_group_create(const int* devices, int G, int combine_mode, chp_group** out) {
     if (!out) return CHP_EINVAL;
+    DeviceGuard keep;
     *out = nullptr;
     if (!devices || G < 1 || G > kMaxShards) return CHP_EINVAL;
     if (combine_mode != CHP_COMBINE_NCCL && combine_mode != CHP_COMBINE_PEER) return CHP_EINVAL;
@@ -235,6 +254,7 @@ int chp_group_create(const int* devices, int G, int combine_mode, chp_group** ou
         }
         // device 0 reads every partial DL over peer memory
         cudaSetDevice(devices[0]);
+        if (cudaEventCreateWithFlags(&g->combined, cudaEventDisableTiming) != cudaSuccess) return bail(CHP_EDEVICE);
         for (int k = 1; k < G; ++k) {
             if (devices[k] == devices[0]) continue;
             int can = 0;
@@ -259,6 +279,7 @@ int chp_group_create(const int* devices, int G, int combine_mode, chp_group** ou
 
 void chp_group_destroy(chp_group* g) {
     if (!g) return;
+    DeviceGuard keep;
     for (int k = 0; k < (int)g->ctx.size(); ++k) chp_ctx_sync(g->ctx[k]);
     if (!g->comm.empty()) {
         const NcclApi& api = nccl();
@@ -270,6 +291,10 @@ void chp_group_destroy(chp_group* g) {
             cudaSetDevice(g->dev[k]);
             cudaEventDestroy(g->folded[k]);
         }
+    if (g->combined) {
+        cudaSetDevice(g->dev[0]);
+        cudaEventDestroy(g->combined);
+    }
     for (chp_ctx* c : g->ctx) chp_ctx_destroy(c);
     delete g;
 }
@@ -285,6 +310,7 @@ uint64_t chp_group_last_h2d_bytes(const chp_group* g) { return g ? g->h2d_bytes 
 int chp_reduce_sharded(chp_group* g, const int32_t* const* d_xy, const uint64_t* n, int64_t width, int64_t q,
                        int32_t* const* d_L) {
     if (!g || !d_xy || !n || !d_L) return CHP_EINVAL;
+    DeviceGuard keep;
     for (int k = 0; k < g->G; ++k) {
         cudaSetDevice(g->dev[k]);
         const int rc = chp_reduce(g->ctx[k], d_xy[k], n[k], width, q, 0, d_L[k], 0);

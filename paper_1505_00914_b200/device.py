@@ -374,10 +374,12 @@ class Group:
             raise ValueError(msg)
         raise ChpError(msg)
 
-    def reduce_sharded(self, shards, width: int, q: int | None = None, outs=None):
+    def reduce_sharded(self, shards, width: int, q: int | None = None, outs=None, sync: bool = True):
         """Device-resident shards (one (n_k, 2) int32 CUDA tensor per group
         device).  Returns the per-shard DLs; DL 0 holds the merged L (NCCL:
-        every DL does).  Runs on each shard context's own stream."""
+        every DL does).  Runs on each shard context's own stream; sync=False
+        returns without waiting for them (chp_reduce_sharded orders later
+        group calls after the combine)."""
         G = self.size
         if len(shards) != G:
             raise ValueError(f"{len(shards)} shards for a group of {G}")
@@ -393,9 +395,13 @@ class Group:
         ns = (ctypes.c_uint64 * G)(*[t.numel() // 2 for t in shards])
         ds = (c_void_p * G)(*[d.data_ptr() for d in outs])
         self._check(self.L.chp_reduce_sharded(self.h, xs, ns, int(width), -1 if q is None else int(q), ds))
-        for k in range(G):
-            self.L.chp_ctx_sync(self.L.chp_group_ctx(self.h, k))
+        if sync:
+            self.sync()
         return outs
+
+    def sync(self):
+        for k in range(self.size):
+            self.L.chp_ctx_sync(self.L.chp_group_ctx(self.h, k))
 
     def pipeline_host(self, xy: np.ndarray, width: int, q: int | None = None, L: bool = False, occ: bool = False,
                       chain: bool = True, hull: bool = False) -> dict:

@@ -20,6 +20,7 @@ import pytest
 import torch
 
 from paper_1505_00914_b200.device import Group, generate_host
+from paper_1505_00914_b200.shard import dl_unpack_host
 
 pytestmark = pytest.mark.gpu
 
@@ -96,6 +97,33 @@ def test_peer_group_reduce_sharded_device_resident(ctx, orc, G):
     assert np.array_equal(comp["lpairs"].cpu().numpy(), L)
     s = int(comp["counts"][0].item())
     assert s == len(chain) and np.array_equal(comp["chain"][:s].cpu().numpy(), chain)
+    g.close()
+
+
+def test_peer_group_back_to_back_calls_share_partials(orc):
+    """Two chp_reduce_sharded calls without a sync between them, the shard
+    partials (d_L[k], k > 0) shared: the second call's DL init on a shard
+    stream must wait for the first call's combine to read that partial."""
+    G, p = 4, 65536
+    xs = [generate_host(2, 2, p, 4_000_000), generate_host(4, 4, p, 4_000_000)]
+    g = Group([0] * G, combine="peer")
+    shared = [torch.empty(int(g.L.chp_dl_len(p)), dtype=torch.int32, device="cuda") for _ in range(G - 1)]
+    heads = [torch.empty(int(g.L.chp_dl_len(p)), dtype=torch.int32, device="cuda") for _ in range(2)]
+    for _ in range(3):
+        outs = []
+        for xy, head in zip(xs, heads):
+            d = torch.from_numpy(xy).cuda()
+            n = len(xy)
+            shards = [d[n * k // G:n * (k + 1) // G].contiguous() for k in range(G)]
+            torch.cuda.synchronize()
+            outs.append(g.reduce_sharded(shards, p, p, outs=[head] + shared, sync=False)[0])
+        g.sync()
+        for xy, DL in zip(xs, outs):
+            arr = orc.reduce(xy, p, p)
+            lo, hi, valid, err = dl_unpack_host(DL.cpu().numpy())
+            assert err == 0
+            L = np.stack([np.where(valid, lo, p + 1), np.where(valid, hi, -1)], axis=1)
+            assert np.array_equal(L, orc.L_pairs(arr))
     g.close()
 
 
