@@ -194,13 +194,24 @@ def cpu_time_sample(cfg: int, n_sample: int, threads: int, reps: int):
     return once, kind, threads
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline(cfg: int, n_sample: int, reps: int = 2):
     once, kind, threads = cpu_time_sample(cfg, n_sample, threads=1, reps=reps)
     t = min(once() for _ in range(reps))
     return {"value": n_sample / t / 1e9, "unit": "Gpoints/s", "cores": threads, "kind": kind,
             "sample": f"first {n_sample:.3g} points of config {cfg} (same bytes as the GPU input), "
                       f"chp::reducer::reduce + build_polyline, best of {reps}, {threads} thread; "
-                      f"host {os.cpu_count()} cpus", "seconds": t}
+                      f"host {os.cpu_count()} cpus", "seconds": t, "host_cpu": cpu_model(), "nproc": os.cpu_count()}
 
 
 def run_reference(args):
@@ -225,7 +236,8 @@ def run_reference(args):
         "cpu_baseline": {"value": value, "unit": "Gpoints/s", "cores": threads, "kind": kind,
                          "sample": f"per step the first {n_sample:.3g} of the config's {n_total:.3g} points "
                                    f"(bounded CPU sample), chp::reducer::reduce per thread chunk + element-wise "
-                                   f"merge + build_polyline, {threads} host threads"},
+                                   f"merge + build_polyline, {threads} host threads",
+                         "host_cpu": cpu_model(), "nproc": os.cpu_count()},
         "e2e": {"value": value, "unit": "Gpoints/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
