@@ -51,7 +51,7 @@ def run(variant, chunks):
         if k == 0:
             fa = fb = None
         else:
-            if gshift == 0:
+            if variant == 'exact':
                 fa, fb = lo.astype(np.int64), hi.astype(np.int64); ys = 0
                 never = lo > hi
                 fa = np.where(never, 1, fa); fb = np.where(never, 0, fb)
@@ -66,7 +66,7 @@ def run(variant, chunks):
                 m = np.ones(len(s), bool)
             else:
                 gi = s >> gshift
-                u = (y - 1) >> ys if gshift else y
+                u = (y - 1) >> ys if variant != 'exact' else y
                 m = ~((u >= fa[gi]) & (u <= fb[gi]))
             ms = s[m]; my = y[m]
             miss_tot += len(ms)
