@@ -15,14 +15,18 @@ pytestmark = pytest.mark.gpu
 SEEDS = int(os.environ.get("CHP_STRESS_SEEDS", "40"))  # a one-off soak: CHP_STRESS_SEEDS=1000
 
 FORCE = [0, _lib.REDUCE_FORCE_GLOBAL, _lib.REDUCE_FORCE_SMEM32, _lib.REDUCE_FORCE_SMEM16,
-         _lib.REDUCE_FORCE_SAMPLED, _lib.REDUCE_FORCE_FILTER, _lib.REDUCE_FORCE_FILTER8]
+         _lib.REDUCE_FORCE_SAMPLED, _lib.REDUCE_FORCE_FILTER, _lib.REDUCE_FORCE_FILTER8,
+         _lib.REDUCE_FORCE_GLOBAL | _lib.REDUCE_WARP_AGG, _lib.REDUCE_FORCE_FILTER | _lib.REDUCE_BLOCKED,
+         _lib.REDUCE_FORCE_SAMPLED | _lib.REDUCE_SAMPLE_SPLIT, _lib.REDUCE_FORCE_FILTER | 128,
+         _lib.REDUCE_FORCE_FILTER | 256 | 4096]
 
 
 def draw_case(rng):
     width = int(rng.choice([1, 2, 7, 64, 257, 4096, 65536, 65537, 300_000, 1 << 20]))
     ywin = rng.choice(["tiny", "16", "20", "none"])
     q = {"tiny": int(rng.integers(1, 50)), "16": 65536, "20": 1 << 20, "none": None}[ywin]
-    n = int(rng.choice([1, 2, 3, 15, 16, 17, 1000, 65_537, 1_000_003, 3_000_001]))
+    # (5 M: past the 4 Mi points where the group filter runs in phases)
+    n = int(rng.choice([1, 2, 3, 15, 16, 17, 1000, 65_537, 1_000_003, 3_000_001, 5_000_001]))
     if rng.random() < 0.5:
         x = rng.integers(1, width + 1, n)
     else:  # a few hot clusters of columns
