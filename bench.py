@@ -257,6 +257,10 @@ class Arm:
         # wrapped onto the visible devices) exists only to exercise the N > 1
         # control flow on a 1-GPU box; it is not a measurement configuration.
         self.backend = os.environ.get("CHP_DIST_BACKEND", "nccl")
+        if self.world > 1 and "CHP_HOST_THREADS" not in os.environ:
+            # the host packing pools of the ranks on this node share its cores
+            local_world = int(os.environ.get("LOCAL_WORLD_SIZE", self.world))
+            os.environ["CHP_HOST_THREADS"] = str(max(2, (os.cpu_count() or 2) // local_world))
         self.local = local % max(torch.cuda.device_count(), 1)
         if self.world > 1:
             torch.cuda.set_device(self.local)

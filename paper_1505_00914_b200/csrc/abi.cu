@@ -112,7 +112,11 @@ class HostPool {
 HostPool* pool_of(chp_ctx* ctx) {
     if (!ctx->pool) {
         const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-        const int parts = ctx->pool_parts > 0 ? ctx->pool_parts : (int)std::min(hw, 32u);
+        int parts = ctx->pool_parts > 0 ? ctx->pool_parts : (int)std::min(hw, 32u);
+        // CHP_HOST_THREADS: the caller's share of the host (e.g. one process
+        // per GPU on a multi-GPU box: cores / local ranks; bench.py sets it)
+        if (const char* e = std::getenv("CHP_HOST_THREADS"))
+            if (std::atoi(e) > 0) parts = std::min(std::atoi(e), 64);
         ctx->pool = new HostPool(std::max(parts, 1) - 1);
     }
     return static_cast<HostPool*>(ctx->pool);
