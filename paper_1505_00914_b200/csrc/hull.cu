@@ -11,10 +11,12 @@
 // reflected through the origin, (-x, -hi) read back to front, whose lower
 // hull is the upper hull rotated by 180 degrees.
 //
-//   leaf   : one thread per chunk of 32 consecutive points runs the strict
-//            monotone chain (pop while cross <= 0).  A point that is not a
-//            strict vertex of its chunk's lower hull lies on or above a
-//            segment between two chunk points, so it is no global vertex.
+//   leaf   : one lane per chunk of 32 consecutive points runs the strict
+//            monotone chain (pop while cross <= 0); a warp loads its 32
+//            chunks together (coalesced) into shared-memory stacks.  A point
+//            that is not a strict vertex of its chunk's lower hull lies on or
+//            above a segment between two chunk points, so it is no global
+//            vertex.
 //   merge  : log2(#chunks) levels; one warp merges two x-separated lower
 //            hulls A | B by their bridge: i* = first i with
 //            Q(i) = [A[i+1] strictly below line A[i] -> tangent(A[i], B)]
@@ -28,8 +30,9 @@
 //            1 or 2 vertices {lexmin, lexmax} as in src/geometry.cpp:29-38.
 // With cooperative launch the three stages are ONE kernel (a grid barrier
 // per merge level); otherwise one launch per stage and level.
-// Orientation tests are exact (__int128 cross products,
-// include/chp/geometry.hpp:29-35).
+// Orientation tests are exact: 64-bit cross products suffice for these
+// inputs (see orient), where the reference needs __int128
+// (include/chp/geometry.hpp:29-35).
 #include <algorithm>
 #include <cstdlib>
 
@@ -43,8 +46,13 @@ struct P {
     long long x, y;
 };
 
+// Exact in 64 bits for K4's inputs: every x lies in one width of at most
+// 2^29 slots and every y is an int32, so |dx| < 2^29, |dy| < 2^32 and each
+// product is below 2^61 (the reference's __int128 form,
+// include/chp/geometry.hpp:29-35, is needed for arbitrary int64 points; the
+// 128-bit multiplies doubled the leaf chain's instruction count).
 __device__ __forceinline__ int orient(const P& a, const P& b, const P& c) {
-    const __int128 v = (__int128)(b.x - a.x) * (c.y - a.y) - (__int128)(b.y - a.y) * (c.x - a.x);
+    const long long v = (b.x - a.x) * (c.y - a.y) - (b.y - a.y) * (c.x - a.x);
     return (v > 0) - (v < 0);
 }
 __device__ __forceinline__ bool peq(const P& a, const P& b) { return a.x == b.x && a.y == b.y; }
@@ -52,41 +60,68 @@ __device__ __forceinline__ bool lex_less(const P& a, const P& b) {
     return a.x < b.x || (a.x == b.x && a.y < b.y);
 }
 
-// Point k of problem `prob`: 0 = lower sequence, 1 = reflected upper.
-__device__ __forceinline__ P seq_point(const int2* lower, const int2* upper, long long v, int prob, long long k) {
-    if (prob == 0) {
-        const int2 q = lower[k];
-        return P{q.x, q.y};
-    }
-    const int2 q = upper[v - 1 - k];
-    return P{-(long long)q.x, -(long long)q.y};
+// The 32 chunks c0 .. c0+31 of problem `prob`, one per lane of the calling
+// warp: the warp loads the chunks' points together (lane l takes point l of
+// every chunk, so each load is one contiguous run -- a thread loading its own
+// chunk strided the warp's loads 256 bytes apart: 32 sectors per load), then
+// each lane runs the strict monotone chain over its chunk in its
+// shared-memory stack (kStride entries: the odd stride keeps the lanes'
+// stacks on different banks).  The stacks hold the points' int32
+// coordinates before the reflection (8 bytes; they always fit), the chain
+// works on the reflected 64-bit values.
+constexpr int kStride = kLeaf + 1;
+__device__ __forceinline__ P from_stack(int2 s, int prob) {
+    return prob ? P{-(long long)s.x, -(long long)s.y} : P{s.x, s.y};
 }
-
-// Chunk c of problem `prob`: the strict monotone chain over its <= 32
-// points, with the stack in shared memory (a global-memory stack put a
-// store->load round trip in every step: 48-54 us at C2/C3).
-__device__ __forceinline__ void leaf_chunk(const int2* __restrict__ lower, const int2* __restrict__ upper, long long v,
-                                           int prob, uint32_t c, uint32_t nchunks, uint64_t cap, P* stack,
-                                           P* __restrict__ buf, int* __restrict__ cnt) {
-    const long long b = (long long)c * kLeaf;
-    int* cp = cnt + (size_t)prob * nchunks + c;
-    if (b >= v) {
-        *cp = 0;
-        return;
+// Problem 0 is `lower` as is, problem 1 `upper` read back to front (and
+// reflected when the points become 64-bit).
+__device__ __forceinline__ void leaf_warp(const int2* __restrict__ lower, const int2* __restrict__ upper, long long v,
+                                          int prob, uint32_t c0, uint32_t nchunks, uint64_t cap, int2* wstack,
+                                          P* __restrict__ buf, int* __restrict__ cnt) {
+    const int lane = threadIdx.x & 31;
+    const long long base = (long long)c0 * kLeaf;
+#pragma unroll
+    for (int j0 = 0; j0 < kLeaf; j0 += 8) {
+        int2 q[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const long long k = base + (long long)(j0 + j) * kLeaf + lane;
+            if (k < v) q[j] = prob ? upper[v - 1 - k] : lower[k];
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) wstack[(j0 + j) * kStride + lane] = q[j];
     }
-    const int m = (int)(min(b + kLeaf, v) - b);
-    // All loads first (in flight together), then the chain in place: the
-    // stack top k never passes the read position i.
-    for (int i = 0; i < m; ++i) stack[i] = seq_point(lower, upper, v, prob, b + i);
-    int k = 0;
-    for (int i = 0; i < m; ++i) {
-        const P q = stack[i];
-        while (k >= 2 && orient(stack[k - 2], stack[k - 1], q) <= 0) --k;
-        stack[k++] = q;
+    __syncwarp();
+    const uint32_t c = c0 + lane;
+    if (c < nchunks) {
+        const long long b = base + (long long)lane * kLeaf;
+        int* cp = cnt + (size_t)prob * nchunks + c;
+        if (b >= v) {
+            *cp = 0;
+        } else {
+            int2* stack = wstack + lane * kStride;
+            const int m = (int)(min(b + kLeaf, v) - b);
+            // the top two entries live in registers
+            P t1{0, 0}, t2{0, 0};
+            int k = 0;
+            for (int i = 0; i < m; ++i) {
+                const int2 qs = stack[i];
+                const P q = from_stack(qs, prob);
+                while (k >= 2 && orient(t2, t1, q) <= 0) {
+                    --k;
+                    t1 = t2;
+                    if (k >= 2) t2 = from_stack(stack[k - 2], prob);
+                }
+                stack[k++] = qs;
+                t2 = t1;
+                t1 = q;
+            }
+            P* out = buf + (size_t)prob * cap + b;
+            for (int i = 0; i < k; ++i) out[i] = from_stack(stack[i], prob);
+            *cp = k;
+        }
     }
-    P* out = buf + (size_t)prob * cap + b;
-    for (int i = 0; i < k; ++i) out[i] = stack[i];
-    *cp = k;
+    __syncwarp();  // the stacks are reused by the warp's next chunks
 }
 
 // First j in [0, nb-1) with orient(q, B[j], B[j+1]) > 0, else nb-1.
@@ -233,21 +268,23 @@ __device__ __forceinline__ void final_block(const P* __restrict__ fin, const int
     if (threadIdx.x == 0) *h_out = h;
 }
 
-constexpr int kLeafThreads = 128;  // leaf threads per CTA: stacks of 128 x 32 x 16 B = 64 KB
-constexpr size_t kLeafSmem = (size_t)kLeafThreads * kLeaf * sizeof(P);
-constexpr int kCoopThreads = 512;
+constexpr int kLeafThreads = 128;  // threads per k_hull_leaf CTA (the multi-launch form)
+constexpr size_t kLeafSmem = (size_t)kLeafThreads * kStride * sizeof(int2);
+constexpr int kCoopThreads = 512;  // every thread of the cooperative form runs leaves
+constexpr size_t kCoopSmem = (size_t)kCoopThreads * kStride * sizeof(int2);  // 132 KB
 constexpr uint32_t kSmallChunks = 64;  // one-CTA form up to 64 chunks per problem
-static_assert((kCoopThreads / 32) * kStage * sizeof(P) <= kLeafSmem, "merge slabs reuse the leaf stacks");
+static_assert((kCoopThreads / 32) * kStage * sizeof(P) <= kCoopSmem, "merge slabs reuse the leaf stacks");
 
 __global__ void __launch_bounds__(kLeafThreads) k_hull_leaf(const int2* __restrict__ lower,
                                                             const int2* __restrict__ upper,
                                                             const long long* __restrict__ counts, uint32_t nchunks,
                                                             uint64_t cap, P* __restrict__ buf,
                                                             int* __restrict__ cnt) {
-    extern __shared__ P stacks[];
-    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= nchunks) return;
-    leaf_chunk(lower, upper, counts[1], blockIdx.y, c, nchunks, cap, stacks + threadIdx.x * kLeaf, buf, cnt);
+    extern __shared__ int2 lstacks[];
+    const uint32_t c0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u);
+    if (c0 >= nchunks) return;
+    leaf_warp(lower, upper, counts[1], blockIdx.y, c0, nchunks, cap, lstacks + (threadIdx.x & ~31u) * kStride, buf,
+              cnt);
 }
 
 __global__ void __launch_bounds__(256) k_hull_merge(const P* __restrict__ in, const int* __restrict__ cnt_in, P* __restrict__ out,
@@ -266,20 +303,25 @@ __global__ void k_hull_final(const P* __restrict__ fin, const int* __restrict__ 
     final_block(fin, cnt_fin, nchunks, cap, counts, swapped, tmp, hull, h_out);
 }
 
-// All of K4 as one cooperative kernel (one CTA per SM): leaves, a grid
-// barrier per merge level (~1.3 us instead of a launch boundary), and the
-// final on CTA 0.
+// All of K4 as one cooperative kernel (one CTA per SM): the leaves (every
+// thread: a warp takes 32 chunks), a grid barrier per merge level (~1.3 us
+// instead of a launch boundary), and the final on CTA 0.  (Rounds of leaf
+// filtering with an in-order compaction between them, until few points are
+// left, measured slower: ~25 us per round against ~7 us per merge level.)
 __global__ void __launch_bounds__(kCoopThreads, 1)
     k_hull_coop(const int2* __restrict__ lower, const int2* __restrict__ upper, const long long* __restrict__ counts,
                 uint32_t nchunks, uint64_t cap, P* buf0, P* buf1, int* cnt0, int* cnt1, int swapped, P* tmp,
                 int2* __restrict__ hull, long long* __restrict__ h_out, GridBar* bar) {
-    extern __shared__ P stacks[];
+    extern __shared__ int2 lstacks[];  // leaf stacks; later the merges' slabs
+    P* stacks = reinterpret_cast<P*>(lstacks);
     const long long v = counts[1];
-    if (threadIdx.x < kLeafThreads) {
-        for (uint32_t t = blockIdx.x * kLeafThreads + threadIdx.x; t < 2 * nchunks; t += gridDim.x * kLeafThreads) {
-            const int prob = t >= nchunks;
-            leaf_chunk(lower, upper, v, prob, prob ? t - nchunks : t, nchunks, cap, stacks + threadIdx.x * kLeaf,
-                       buf0, cnt0);
+    {  // warp tasks: 32 chunks of one problem each
+        const uint32_t nwc = (nchunks + 31) / 32;
+        const uint32_t lw = threadIdx.x >> 5, nlw = blockDim.x / 32;
+        for (uint32_t t = blockIdx.x * nlw + lw; t < 2 * nwc; t += gridDim.x * nlw) {
+            const int prob = t >= nwc;
+            leaf_warp(lower, upper, v, prob, (prob ? t - nwc : t) * 32, nchunks, cap,
+                      lstacks + (threadIdx.x & ~31u) * kStride, buf0, cnt0);
         }
     }
     // (a single CTA -- small widths, launched plainly -- needs no grid barrier)
@@ -336,10 +378,10 @@ extern "C" int chp_hull(chp_ctx* ctx, const int32_t* d_lower, const int32_t* d_u
     if (nchunks <= kSmallChunks && !force_launches) {
         if (!ctx->hull_small_attr) {
             CHP_CUDA(ctx, cudaFuncSetAttribute(k_hull_coop, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)kLeafSmem));
+                                               (int)kCoopSmem));
             ctx->hull_small_attr = 1;
         }
-        k_hull_coop<<<1, kCoopThreads, kLeafSmem, ctx->stream>>>(
+        k_hull_coop<<<1, kCoopThreads, kCoopSmem, ctx->stream>>>(
             reinterpret_cast<const int2*>(d_lower), reinterpret_cast<const int2*>(d_upper), counts, nchunks, cap,
             bufs[0], bufs[1], cnts[0], cnts[1], swapped, tmp, reinterpret_cast<int2*>(d_hull),
             reinterpret_cast<long long*>(d_h), nullptr);
@@ -354,9 +396,9 @@ extern "C" int chp_hull(chp_ctx* ctx, const int32_t* d_lower, const int32_t* d_u
         if (!ctx->hull_coop_checked) {
             ctx->hull_coop_checked = 1;
             int per_sm = 0;
-            if (cudaFuncSetAttribute(k_hull_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLeafSmem) ==
+            if (cudaFuncSetAttribute(k_hull_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCoopSmem) ==
                     cudaSuccess &&
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hull_coop, kCoopThreads, kLeafSmem) ==
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hull_coop, kCoopThreads, kCoopSmem) ==
                     cudaSuccess)
                 ctx->hull_coop_ok = per_sm >= 1;
             cudaGetLastError();
@@ -370,16 +412,16 @@ extern "C" int chp_hull(chp_ctx* ctx, const int32_t* d_lower, const int32_t* d_u
             uint32_t nc = nchunks;
             uint64_t cp = cap;
             int sw = swapped;
-            void* args[] = {(void*)&lo,      (void*)&up,      (void*)&counts, (void*)&nc,   (void*)&cp,
+            void* args[] = {(void*)&lo,      (void*)&up,      (void*)&counts,  (void*)&nc,   (void*)&cp,
                             (void*)&bufs[0], (void*)&bufs[1], (void*)&cnts[0], (void*)&cnts[1], (void*)&sw,
-                            (void*)&tmp,     (void*)&hp,      (void*)&hh,     (void*)&bar};
+                            (void*)&tmp,     (void*)&hp,      (void*)&hh,      (void*)&bar};
             // (Refused when the grid cannot be co-resident: the launches below.)
             // CHP_TEST_COOP_REFUSE (tests): an oversized grid, which the
             // runtime refuses without running anything.
             static const bool refuse = getenv("CHP_TEST_COOP_REFUSE") != nullptr;
             if (cudaLaunchCooperativeKernel((const void*)k_hull_coop, dim3(ctx->sm_count * (refuse ? 64 : 1)),
                                             dim3(kCoopThreads), args,
-                                            kLeafSmem, ctx->stream) == cudaSuccess) {
+                                            kCoopSmem, ctx->stream) == cudaSuccess) {
                 CHP_LAUNCHED(ctx);
                 return CHP_OK;
             }
@@ -414,3 +456,4 @@ extern "C" int chp_hull(chp_ctx* ctx, const int32_t* d_lower, const int32_t* d_u
     CHP_LAUNCHED(ctx);
     return CHP_OK;
 }
+
