@@ -330,14 +330,22 @@ __global__ void __launch_bounds__(kCoopThreads, 1)
     int *cin = cnt0, *cout = cnt1;
     uint32_t nregions = nchunks;
     uint64_t region_cap = kLeaf;
-    const uint32_t warps = gridDim.x * (blockDim.x >> 5);
-    const uint32_t gw0 = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    bool alone = gridDim.x == 1;
     while (nregions > 1) {
         const uint32_t npairs = (nregions + 1) / 2;
+        // The last levels (at most one pair per warp of a CTA) on CTA 0
+        // alone, with block barriers instead of grid barriers.
+        if (!alone && 2 * npairs <= (blockDim.x >> 5)) {
+            grid_barrier_done(bar);
+            if (blockIdx.x != 0) return;
+            alone = true;
+        }
+        const uint32_t warps = (alone ? 1u : gridDim.x) * (blockDim.x >> 5);
+        const uint32_t gw0 = (alone ? 0u : blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
         for (uint32_t gw = gw0; gw < 2 * npairs; gw += warps)
             merge_pair(gw, threadIdx.x & 31, bin, cin, bout, cout, nchunks, cap, nregions, region_cap,
                        stacks + (threadIdx.x >> 5) * kStage);  // the leaf stacks, free after the leaves
-        if (gridDim.x == 1) __syncthreads(); else grid_barrier(bar);
+        if (alone) __syncthreads(); else grid_barrier(bar);
         P* tb = bin;
         bin = bout;
         bout = tb;
@@ -347,7 +355,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1)
         nregions = npairs;
         region_cap *= 2;
     }
-    if (gridDim.x > 1) grid_barrier_done(bar);
+    if (!alone) grid_barrier_done(bar);
     if (blockIdx.x == 0) final_block(bin, cin, nchunks, cap, counts, swapped, tmp, hull, h_out);
 }
 
