@@ -1688,7 +1688,9 @@ int chp_reduce_yr(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int64_t width, 
             // (CHP_REDUCE_SAMPLE_PREFIX).  C2, same box: n * 32/256 585-590,
             // 24/256 596, 20/256 612, 16/256 631, 14/256 638, 12/256 619,
             // 10/256 620, 8/256 600 Gpts/s (k = 3 had been best before the
-            // main pass got cheaper per point).
+            // main pass got cheaper per point).  Round 2, K1 us: 11/256 157.4,
+            // 12/256 156.1, 13/256 149.5, 14/256 148.9, 15/256 148.8, 16/256
+            // 149.0, 18/256 150.0 -- flat from 13/256 to 16/256.
             uint32_t f256 = 256u >> ((flags >> 16) & 7 ? (flags >> 16) & 7 : 4);
             int prefix = (flags & CHP_REDUCE_SAMPLE_PREFIX) ? 1 : 0;
             // Default: sample pass + merge as ONE cooperative kernel (a grid
