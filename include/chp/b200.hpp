@@ -14,7 +14,8 @@ namespace chp::b200 {
 // ncclAllReduce when `nccl` (distinct devices), else one peer-memory kernel
 // on the first device.  The result is the single-device result bit for bit.
 // The default comes from CHP_DEVICES ("0,1,2,3"; CHP_COMBINE=peer selects
-// the peer combine), else {CHP_DEVICE or 0}.  Per host thread, like the
+// the peer combine, CHP_COMBINE=fused the shards folding straight into the
+// first device's L over peer memory), else {CHP_DEVICE or 0}.  Per host thread, like the
 // drop-in's device context.
 void use_devices(const std::vector<int>& devices, bool nccl = true);
 std::vector<int> devices();

@@ -258,9 +258,13 @@ int chp_bounds_host64(chp_ctx* ctx, const int64_t* h_xy, uint64_t n, int64_t* h_
  *                     is loaded on first use)
  *   CHP_COMBINE_PEER  device 0 waits on every shard's K1 and one kernel
  *                     reads the partial DLs over peer memory (NVLink P2P);
- *                     devices may repeat (G contexts on one device). */
+ *                     devices may repeat (G contexts on one device).
+ *   CHP_COMBINE_FUSED every shard's K1 folds straight into device 0's DL
+ *                     over peer memory (NVLink atomics), no combine step;
+ *                     only d_L[0] is used; devices may repeat. */
 #define CHP_COMBINE_NCCL 0
 #define CHP_COMBINE_PEER 1
+#define CHP_COMBINE_FUSED 2
 typedef struct chp_group chp_group;
 int chp_group_create(const int* devices, int G, int combine, chp_group** out);
 void chp_group_destroy(chp_group* g);

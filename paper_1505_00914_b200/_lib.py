@@ -12,7 +12,7 @@ from ctypes import POINTER, c_char_p, c_int, c_int32, c_int64, c_uint32, c_uint6
 from ._build import LIB
 
 CHP_OK, CHP_EINVAL, CHP_EDEVICE = 0, 1, 2
-COMBINE_NCCL, COMBINE_PEER = 0, 1
+COMBINE_NCCL, COMBINE_PEER, COMBINE_FUSED = 0, 1, 2
 REDUCE_ACCUMULATE = 1
 REDUCE_NO_VALIDATE = 2
 REDUCE_FORCE_GLOBAL = 4

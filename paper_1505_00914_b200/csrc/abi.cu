@@ -896,7 +896,8 @@ int chp_pipeline_host64(chp_ctx* ctx, const int64_t* h_xy, uint64_t n, int64_t w
     return pipeline_core(ctx, in, n, width, q, h_Lpairs, h_occ, h_chain, h_s, h_hull, h_h);
 }
 
-static int reduce_host_core(chp_ctx* ctx, const HostPts& in, uint64_t n, int64_t width, int64_t q, int32_t* d_L) {
+static int reduce_host_core(chp_ctx* ctx, const HostPts& in, uint64_t n, int64_t width, int64_t q, int32_t* d_L,
+                            bool init = true) {
     if (!ctx || !d_L) return CHP_EINVAL;
     ctx->h2d_bytes = 0;
     ctx->last_valid = false;
@@ -904,7 +905,7 @@ static int reduce_host_core(chp_ctx* ctx, const HostPts& in, uint64_t n, int64_t
     if (width > (1ll << 29)) return chp_einval(ctx, "reduce: width exceeds the device limit 2^29");
     CHP_CUDA(ctx, cudaSetDevice(ctx->device));
     int rc;
-    if ((rc = chp_dl_init(ctx, d_L, width))) return rc;
+    if (init && (rc = chp_dl_init(ctx, d_L, width))) return rc;
     if ((rc = stream_reduce(ctx, in, n, width, 1, q, 0, 0, d_L))) return rc;
     CHP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     return CHP_OK;
@@ -920,6 +921,20 @@ int chp_reduce_host64(chp_ctx* ctx, const int64_t* h_xy, uint64_t n, int64_t wid
     HostPts in;
     in.p64 = h_xy;
     return reduce_host_core(ctx, in, n, width, q, d_L);
+}
+
+// Shard groups (shard.cu), CHP_COMBINE_FUSED: fold host points into a DL
+// that is already initialised (possibly another device's, over peer memory).
+int chp_reduce_host_into(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t width, int64_t q, int32_t* d_L) {
+    HostPts in;
+    in.p32 = h_xy;
+    return reduce_host_core(ctx, in, n, width, q, d_L, false);
+}
+
+int chp_reduce_host64_into(chp_ctx* ctx, const int64_t* h_xy, uint64_t n, int64_t width, int64_t q, int32_t* d_L) {
+    HostPts in;
+    in.p64 = h_xy;
+    return reduce_host_core(ctx, in, n, width, q, d_L, false);
 }
 
 int chp_finish_host(chp_ctx* ctx, const int32_t* d_L, int64_t width, int32_t* h_Lpairs, uint64_t* h_occ,

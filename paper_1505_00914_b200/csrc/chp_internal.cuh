@@ -127,6 +127,14 @@ static inline int chp_ensure(chp_ctx* ctx, DevBuf& b, size_t bytes) {
     return CHP_OK;
 }
 
+// Host points folded into an initialised DL (abi.cu; shard groups'
+// CHP_COMBINE_FUSED, where the DL is shard 0's, read and REDed over peer
+// memory by the other devices).  extern "C" linkage, not in the header.
+extern "C" int chp_reduce_host_into(chp_ctx* ctx, const int32_t* h_xy, uint64_t n, int64_t width, int64_t q,
+                                    int32_t* d_L);
+extern "C" int chp_reduce_host64_into(chp_ctx* ctx, const int64_t* h_xy, uint64_t n, int64_t width, int64_t q,
+                                      int32_t* d_L);
+
 // K0 pieces used by the host pipelines (misc.cu).
 int chp_bounds_init(chp_ctx* ctx, int32_t* d_out4);
 int chp_bounds_accumulate(chp_ctx* ctx, const int32_t* d_xy, uint64_t n, int32_t* d_out4);

@@ -62,6 +62,7 @@ void check(int rc) {
 struct GroupHolder {
     std::vector<int> devices;
     bool nccl = true;
+    bool fused = false;  // CHP_COMBINE=fused: the shards fold into device 0's L over peer memory
     bool configured = false;
     chp_group* group = nullptr;
     ~GroupHolder() {
@@ -85,7 +86,8 @@ GroupHolder& group_holder() {
             }
         }
         const char* comb = std::getenv("CHP_COMBINE");
-        h.nccl = !(comb && std::string(comb) == "peer");
+        h.nccl = !(comb && (std::string(comb) == "peer" || std::string(comb) == "fused"));
+        h.fused = comb && std::string(comb) == "fused";
     }
     return h;
 }
@@ -96,7 +98,8 @@ chp_group* group() {
     if (h.devices.size() < 2) return nullptr;
     if (!h.group) {
         const int rc = chp_group_create(h.devices.data(), static_cast<int>(h.devices.size()),
-                                        h.nccl ? CHP_COMBINE_NCCL : CHP_COMBINE_PEER, &h.group);
+                                        h.nccl ? CHP_COMBINE_NCCL : h.fused ? CHP_COMBINE_FUSED : CHP_COMBINE_PEER,
+                                        &h.group);
         if (rc == CHP_EINVAL) throw std::invalid_argument("chp: bad device list for the shard group");
         if (rc != CHP_OK) throw std::runtime_error("chp: shard group creation failed");
     }

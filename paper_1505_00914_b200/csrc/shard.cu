@@ -17,6 +17,14 @@
 //                     (P2P loads through NVLink) into DL 0.  Devices may
 //                     repeat: G contexts on one device run the same code path
 //                     (how the 1-GPU test box exercises G > 1).
+//   CHP_COMBINE_FUSED no partial DLs and no combine step: device 0
+//                     initialises DL 0 and every shard's K1 folds straight
+//                     into it over peer memory (its flush and miss-path REDs
+//                     are NVLink atomics on device 0's L2), so the exchange
+//                     happens inside K1, overlapped with the other shards'
+//                     streams.  Best where K1 touches L little (shared-memory
+//                     tables flushed once per CTA: C5's 256 columns); every
+//                     L2 access of a filter variant becomes remote.
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -94,7 +102,8 @@ struct chp_group {
     std::vector<chp_ctx*> ctx;
     std::vector<ncclComm_t> comm;
     std::vector<cudaEvent_t> folded;  // per shard: its partial DL is complete
-    cudaEvent_t combined = nullptr;   // (peer) the combine kernel has read every partial
+    cudaEvent_t combined = nullptr;   // (peer) the combine kernel has read every partial;
+                                      // (fused) DL 0 is initialised
     std::string err;
     uint64_t h2d_bytes = 0;
 };
@@ -122,7 +131,19 @@ void slice(uint64_t n, int G, int k, uint64_t* lo, uint64_t* cnt) {
 // the element-wise MIN.  Stream-ordered after each shard's K1.
 int combine(chp_group* g, int32_t* const* d_L, int64_t width) {
     const uint64_t words = chp_dl_len(width);
-    if (g->G == 1 && g->combine == CHP_COMBINE_PEER) return CHP_OK;
+    if (g->G == 1 && g->combine != CHP_COMBINE_NCCL) return CHP_OK;
+    if (g->combine == CHP_COMBINE_FUSED) {  // DL 0 already holds everything: device 0 waits for the shards
+        for (int k = 1; k < g->G; ++k) {
+            cudaSetDevice(g->dev[k]);
+            if (cudaEventRecord(g->folded[k], g->ctx[k]->stream) != cudaSuccess)
+                return gfail(g, CHP_EDEVICE, "cudaEventRecord");
+        }
+        cudaSetDevice(g->dev[0]);
+        for (int k = 1; k < g->G; ++k)
+            if (cudaStreamWaitEvent(g->ctx[0]->stream, g->folded[k], 0) != cudaSuccess)
+                return gfail(g, CHP_EDEVICE, "cudaStreamWaitEvent");
+        return CHP_OK;
+    }
     if (g->combine == CHP_COMBINE_NCCL) {
         const NcclApi& api = nccl();
         ncclResult_t r = api.groupStart();
@@ -172,6 +193,21 @@ struct DeviceGuard {
     ~DeviceGuard() { cudaSetDevice(dev); }
 };
 
+// CHP_COMBINE_FUSED: DL 0 initialised on device 0, every shard stream
+// ordered after it.
+int fused_init(chp_group* g, int32_t* dl0, int64_t width) {
+    cudaSetDevice(g->dev[0]);
+    int rc = chp_dl_init(g->ctx[0], dl0, width);
+    if (rc) return gctx_fail(g, 0, rc);
+    if (cudaEventRecord(g->combined, g->ctx[0]->stream) != cudaSuccess) return gfail(g, CHP_EDEVICE, "cudaEventRecord");
+    for (int k = 1; k < g->G; ++k) {
+        cudaSetDevice(g->dev[k]);
+        if (cudaStreamWaitEvent(g->ctx[k]->stream, g->combined, 0) != cudaSuccess)
+            return gfail(g, CHP_EDEVICE, "cudaStreamWaitEvent");
+    }
+    return CHP_OK;
+}
+
 template <typename T>
 int pipeline_sharded(chp_group* g, const T* h_xy, uint64_t n, int64_t width, int64_t q, int32_t* h_Lpairs,
                      uint64_t* h_occ, int32_t* h_chain, int64_t* h_s, int32_t* h_hull, int64_t* h_h) {
@@ -181,12 +217,21 @@ int pipeline_sharded(chp_group* g, const T* h_xy, uint64_t n, int64_t width, int
     if (width < 1) return gfail(g, CHP_EINVAL, "reduce: width must be >= 1");
     if (width > (1ll << 29)) return gfail(g, CHP_EINVAL, "reduce: width exceeds the device limit 2^29");
     std::vector<int32_t*> dl(g->G);
+    const bool fused = g->combine == CHP_COMBINE_FUSED;
     for (int k = 0; k < g->G; ++k) {
         chp_ctx* c = g->ctx[k];
         cudaSetDevice(c->device);
+        if (fused && k > 0) {  // every shard folds into shard 0's DL
+            dl[k] = dl[0];
+            continue;
+        }
         const int rc = chp_ensure(c, c->dl, chp_dl_len(width) * 4);
         if (rc) return gctx_fail(g, k, rc);
         dl[k] = (int32_t*)c->dl.p;
+    }
+    if (fused) {
+        const int rc = fused_init(g, dl[0], width);
+        if (rc) return rc;
     }
     // One host thread per shard: each streams its slice (chunked H2D, packed
     // where the range allows) into its device's partial DL.
@@ -195,9 +240,11 @@ int pipeline_sharded(chp_group* g, const T* h_xy, uint64_t n, int64_t width, int
         uint64_t lo, cnt;
         slice(n, g->G, k, &lo, &cnt);
         if constexpr (sizeof(T) == 4)
-            rcs[k] = chp_reduce_host(g->ctx[k], h_xy + 2 * lo, cnt, width, q, dl[k]);
+            rcs[k] = fused ? chp_reduce_host_into(g->ctx[k], h_xy + 2 * lo, cnt, width, q, dl[k])
+                           : chp_reduce_host(g->ctx[k], h_xy + 2 * lo, cnt, width, q, dl[k]);
         else
-            rcs[k] = chp_reduce_host64(g->ctx[k], h_xy + 2 * lo, cnt, width, q, dl[k]);
+            rcs[k] = fused ? chp_reduce_host64_into(g->ctx[k], h_xy + 2 * lo, cnt, width, q, dl[k])
+                           : chp_reduce_host64(g->ctx[k], h_xy + 2 * lo, cnt, width, q, dl[k]);
     };
     std::vector<std::thread> th;
     for (int k = 1; k < g->G; ++k) th.emplace_back(work, k);
@@ -223,7 +270,8 @@ int chp_group_create(const int* devices, int G, int combine_mode, chp_group** ou
     DeviceGuard keep;
     *out = nullptr;
     if (!devices || G < 1 || G > kMaxShards) return CHP_EINVAL;
-    if (combine_mode != CHP_COMBINE_NCCL && combine_mode != CHP_COMBINE_PEER) return CHP_EINVAL;
+    if (combine_mode != CHP_COMBINE_NCCL && combine_mode != CHP_COMBINE_PEER && combine_mode != CHP_COMBINE_FUSED)
+        return CHP_EINVAL;
     chp_group* g = new chp_group();
     g->G = G;
     g->combine = combine_mode;
@@ -245,22 +293,26 @@ int chp_group_create(const int* devices, int G, int combine_mode, chp_group** ou
         c->pool_parts = (int)std::max(2u, std::min(hw, 32u) / (unsigned)G);
         g->ctx.push_back(c);
     }
-    if (combine_mode == CHP_COMBINE_PEER) {
+    if (combine_mode != CHP_COMBINE_NCCL) {  // peer or fused: events and peer access to device 0
         g->folded.resize(G, nullptr);
         for (int k = 0; k < G; ++k) {
             cudaSetDevice(devices[k]);
             if (cudaEventCreateWithFlags(&g->folded[k], cudaEventDisableTiming) != cudaSuccess)
                 return bail(CHP_EDEVICE);
         }
-        // device 0 reads every partial DL over peer memory
+        // peer: device 0 reads every partial DL; fused: every device
+        // reads and REDs device 0's DL
         cudaSetDevice(devices[0]);
         if (cudaEventCreateWithFlags(&g->combined, cudaEventDisableTiming) != cudaSuccess) return bail(CHP_EDEVICE);
         for (int k = 1; k < G; ++k) {
             if (devices[k] == devices[0]) continue;
+            const int from = combine_mode == CHP_COMBINE_PEER ? devices[0] : devices[k];
+            const int to = combine_mode == CHP_COMBINE_PEER ? devices[k] : devices[0];
             int can = 0;
-            cudaDeviceCanAccessPeer(&can, devices[0], devices[k]);
+            cudaDeviceCanAccessPeer(&can, from, to);
             if (!can) return bail(CHP_EDEVICE);
-            const cudaError_t e = cudaDeviceEnablePeerAccess(devices[k], 0);
+            cudaSetDevice(from);
+            const cudaError_t e = cudaDeviceEnablePeerAccess(to, 0);
             if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return bail(CHP_EDEVICE);
             cudaGetLastError();
         }
@@ -311,9 +363,16 @@ int chp_reduce_sharded(chp_group* g, const int32_t* const* d_xy, const uint64_t*
                        int32_t* const* d_L) {
     if (!g || !d_xy || !n || !d_L) return CHP_EINVAL;
     DeviceGuard keep;
+    const bool fused = g->combine == CHP_COMBINE_FUSED;
+    if (fused) {
+        if (width < 1 || width > (int64_t)INT32_MAX) return gfail(g, CHP_EINVAL, "reduce: width out of range");
+        int rc = fused_init(g, d_L[0], width);
+        if (rc) return rc;
+    }
     for (int k = 0; k < g->G; ++k) {
         cudaSetDevice(g->dev[k]);
-        const int rc = chp_reduce(g->ctx[k], d_xy[k], n[k], width, q, 0, d_L[k], 0);
+        const int rc = fused ? chp_reduce(g->ctx[k], d_xy[k], n[k], width, q, 0, d_L[0], CHP_REDUCE_ACCUMULATE)
+                             : chp_reduce(g->ctx[k], d_xy[k], n[k], width, q, 0, d_L[k], 0);
         if (rc) return gctx_fail(g, k, rc);
     }
     return combine(g, d_L, width);

@@ -327,13 +327,15 @@ class Context:
 class Group:
     """A shard group (include/chp_b200.h chp_group_*): reduce over G devices
     of this box in one process, partial Ls merged by ONE element-wise MIN --
-    ncclAllReduce (combine="nccl", distinct devices) or one peer-memory
-    kernel on device 0 (combine="peer"; devices may repeat)."""
+    ncclAllReduce (combine="nccl", distinct devices), one peer-memory
+    kernel on device 0 (combine="peer"; devices may repeat), or no combine
+    step at all: every shard's K1 folds straight into device 0's DL over
+    peer memory (combine="fused"; only DL 0 is used)."""
 
     def __init__(self, devices, combine: str = "nccl"):
         self.L = _lib.load()
         devs = (ctypes.c_int * len(devices))(*[int(d) for d in devices])
-        mode = {"nccl": _lib.COMBINE_NCCL, "peer": _lib.COMBINE_PEER}[combine]
+        mode = {"nccl": _lib.COMBINE_NCCL, "peer": _lib.COMBINE_PEER, "fused": _lib.COMBINE_FUSED}[combine]
         h = c_void_p()
         rc = self.L.chp_group_create(devs, len(devices), mode, byref(h))
         if rc != CHP_OK:

@@ -35,9 +35,10 @@ def oracle_result(orc, xy, p, q):
 
 @pytest.mark.parametrize("G", [1, 2, 3, 4])
 @pytest.mark.parametrize("config,p,n", [(2, 65536, 5_000_003), (4, 1 << 20, 6_000_001), (5, 256, 4_000_000)])
-def test_peer_group_pipeline_host(orc, G, config, p, n):
+@pytest.mark.parametrize("combine", ["peer", "fused"])
+def test_peer_group_pipeline_host(orc, G, config, p, n, combine):
     xy = generate_host(config, config, p, n)
-    g = Group([0] * G, combine="peer")
+    g = Group([0] * G, combine=combine)
     got = g.pipeline_host(xy, p, p, L=True, chain=True, hull=True)
     L, chain, hull = oracle_result(orc, xy, p, p)
     assert np.array_equal(got["L"], L)
@@ -83,13 +84,14 @@ def test_nccl_group_rejects_repeated_device():
 
 
 @pytest.mark.parametrize("G", [2, 4])
-def test_peer_group_reduce_sharded_device_resident(ctx, orc, G):
+@pytest.mark.parametrize("combine", ["peer", "fused"])
+def test_peer_group_reduce_sharded_device_resident(ctx, orc, G, combine):
     p, n = 16384, 7_000_001
     xy = generate_host(3, 3, p, n)
     d = torch.from_numpy(xy).cuda()
     bounds = [(n * k // G, n * (k + 1) // G) for k in range(G)]
     shards = [d[a:b].contiguous() for a, b in bounds]
-    g = Group([0] * G, combine="peer")
+    g = Group([0] * G, combine=combine)
     DL = g.reduce_sharded(shards, p, p)[0]
     comp = ctx.compact(DL, p, chain=True, lpairs=True)
     torch.cuda.synchronize()
@@ -100,13 +102,14 @@ def test_peer_group_reduce_sharded_device_resident(ctx, orc, G):
     g.close()
 
 
-def test_peer_group_back_to_back_calls_share_partials(orc):
+@pytest.mark.parametrize("combine", ["peer", "fused"])
+def test_peer_group_back_to_back_calls_share_partials(orc, combine):
     """Two chp_reduce_sharded calls without a sync between them, the shard
     partials (d_L[k], k > 0) shared: the second call's DL init on a shard
     stream must wait for the first call's combine to read that partial."""
     G, p = 4, 65536
     xs = [generate_host(2, 2, p, 4_000_000), generate_host(4, 4, p, 4_000_000)]
-    g = Group([0] * G, combine="peer")
+    g = Group([0] * G, combine=combine)
     shared = [torch.empty(int(g.L.chp_dl_len(p)), dtype=torch.int32, device="cuda") for _ in range(G - 1)]
     heads = [torch.empty(int(g.L.chp_dl_len(p)), dtype=torch.int32, device="cuda") for _ in range(2)]
     for _ in range(3):
@@ -127,12 +130,13 @@ def test_peer_group_back_to_back_calls_share_partials(orc):
     g.close()
 
 
-def test_peer_group_error_in_one_shard():
+@pytest.mark.parametrize("combine", ["peer", "fused"])
+def test_peer_group_error_in_one_shard(combine):
     """An invalid coordinate in the last shard sets that partial's error
     word; the MIN combine carries it, and the call raises like reduce()."""
     xy = generate_host(5, 5, 256, 1_000_000)
     xy[-3] = (300, 5)  # x > width
-    g = Group([0, 0, 0], combine="peer")
+    g = Group([0, 0, 0], combine=combine)
     with pytest.raises(ValueError):
         g.pipeline_host(xy, 256, 256)
     xy[-3] = (3, 5)
