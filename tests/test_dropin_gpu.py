@@ -33,3 +33,13 @@ def test_dropin_reference_kats(ctx, lib):
     print(r.stdout[-4000:])
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
     assert "0 failed" in r.stdout
+
+
+@pytest.mark.gpu
+def test_dropin_reference_kats_fused_groups(ctx, lib):
+    """The same, with the drop-in's multi-device reduce on fused shard
+    groups (CHP_COMBINE=fused: the shards fold into the first device's L)."""
+    exe = build_driver(lib)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600, env={**os.environ, "CHP_COMBINE": "fused"})
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    assert "0 failed" in r.stdout
