@@ -167,3 +167,40 @@ def test_bench_two_ranks_gloo_verified(config, n):
     assert line["n_gpus"] == 2 and line["verified"] is True
     assert line["config"]["n_total"] == n and line["result"]["n_per_rank"] == n // 2
     assert line["e2e"]["value"] > 0 and line["gpu_launches"] > 0
+
+
+@pytest.mark.parametrize("combine", ["peer", "fused"])
+@pytest.mark.parametrize("config", [4, 5])
+def test_full_size_sharded_vs_oracle(ctx, orc, combine, config):
+    """BASELINE.json's full C4 (1e9 points) / C5 (4e9 points, "sharded over
+    1/2/4/8 GPUs") as north_star (d) splits it: four contiguous equal
+    shards, each reduced by its own group context, merged by the peer kernel
+    or folded straight into shard 0's L; the merged L and chain against the
+    chunked oracle over all n points (generated on the host, chunk by
+    chunk, from the same counter-based generator)."""
+    import bench
+
+    n, p, seed, _ = bench.CONFIGS[config]
+    free = torch.cuda.mem_get_info()[0]
+    if n * 8 + (2 << 30) > free:
+        pytest.skip("not enough device memory")
+    G = 4
+    bounds = [(n * k // G, n * (k + 1) // G) for k in range(G)]
+    shards = [ctx.generate(config, seed, p, b - a, offset=a) for a, b in bounds]
+    torch.cuda.synchronize()
+    g = Group([0] * G, combine=combine)
+    DL = g.reduce_sharded(shards, p, p)[0]
+    comp = ctx.compact(DL, p, chain=True, lpairs=True)
+    torch.cuda.synchronize()
+    s = int(comp["counts"][0].item())
+    assert int(comp["counts"][2].item()) == 0
+    got_L, got_chain = comp["lpairs"].cpu().numpy(), comp["chain"][:s].cpu().numpy()
+    del shards, comp
+    g.close()
+    acc = orc.accumulator(p, p)
+    chunk = 1 << 26
+    for a in range(0, n, chunk):
+        acc.add(generate_host(config, seed, p, min(chunk, n - a), offset=a))
+    arr = acc.finish()
+    assert np.array_equal(got_L, orc.L_pairs(arr))
+    assert np.array_equal(got_chain, orc.build_polyline(arr))
