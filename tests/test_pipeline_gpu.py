@@ -385,3 +385,32 @@ def test_reduce_host_finish_host_halves(ctx, orc, config, p, pinned):
     c = ctx.reduce_host(bad, p, p)  # no raise here: the error word stays in the DL
     with pytest.raises(ValueError):
         ctx.finish_host(torch.minimum(a, c), p)
+
+
+@pytest.mark.parametrize("config", [4, 5])
+def test_full_size_host_pipeline_vs_oracle(ctx, orc, config):
+    """bench.py's end-to-end path at BASELINE.json size: the whole config
+    (C4 1e9, C5 4e9 points) in pinned host memory through chp_pipeline_host
+    (packed chunks from the host threads plus int32 chunks DMA'd from the
+    input's end), L and chain against the chunked oracle over the same
+    bytes."""
+    import bench
+
+    n, p, seed, _ = bench.CONFIGS[config]
+    with open("/proc/meminfo") as f:
+        avail = next(int(line.split()[1]) * 1024 for line in f if line.startswith("MemAvailable:"))
+    if avail < n * 8 + (8 << 30):
+        pytest.skip(f"needs {(n * 8 + (8 << 30)) / 2**30:.0f} GiB of available host RAM")
+    host = torch.empty((n, 2), dtype=torch.int32, pin_memory=True)
+    chunk = 1 << 27
+    for a in range(0, n, chunk):  # the device generator, copied out chunk by chunk
+        m = min(chunk, n - a)
+        host[a:a + m].copy_(ctx.generate(config, seed, p, m, offset=a))
+    hn = host.numpy()
+    out = ctx.pipeline_host(hn, p, p, L=True, chain=True)
+    acc = orc.accumulator(p, p)
+    for a in range(0, n, chunk):
+        acc.add(hn[a:a + chunk])
+    arr = acc.finish()
+    assert np.array_equal(out["L"], orc.L_pairs(arr))
+    assert np.array_equal(out["chain"], orc.build_polyline(arr))
