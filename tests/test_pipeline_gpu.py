@@ -387,10 +387,10 @@ def test_reduce_host_finish_host_halves(ctx, orc, config, p, pinned):
         ctx.finish_host(torch.minimum(a, c), p)
 
 
-@pytest.mark.parametrize("config", [4, 5])
+@pytest.mark.parametrize("config", [2, 3, 4, 5])
 def test_full_size_host_pipeline_vs_oracle(ctx, orc, config):
     """bench.py's end-to-end paths at BASELINE.json size: the whole config
-    (C4 1e9, C5 4e9 points) in pinned host memory through chp_pipeline_host
+    (C2 1e8, C3 1e9, C4 1e9, C5 4e9 points) in pinned host memory through chp_pipeline_host
     (packed chunks from the host threads plus int32 chunks DMA'd from the
     input's end) and through chp_precondition_run, L, chain and hull against
     the chunked oracle over the same bytes."""
@@ -416,11 +416,12 @@ def test_full_size_host_pipeline_vs_oracle(ctx, orc, config):
     chain = orc.build_polyline(arr)
     assert np.array_equal(out["chain"], chain)
     # reducer::precondition (bounds unknown: one pass folds the bounds while
-    # the chunks land) on the same pinned input: these configs fill their
-    # p x p box, so its L and chain are reduce's and the hull the oracle's
+    # the chunks land) on the same pinned input: when the points fill their
+    # p x p box its L and chain are reduce's and the hull the oracle's
     pre = ctx.precondition_host(hn, chain=True, hull=True)
-    lo = hn[:, 0].min(), hn[:, 1].min()
-    assert pre["bbox"][0] == 1 and lo == (1, 1), (pre["bbox"], lo)
-    assert pre["width"] == p
-    assert np.array_equal(pre["chain"], chain)
-    assert np.array_equal(pre["hull"], orc.melkman(chain))
+    box = (int(hn[:, 0].min()), int(hn[:, 0].max()), int(hn[:, 1].min()), int(hn[:, 1].max()))
+    assert pre["bbox"] == box
+    if box == (1, p, 1, p):  # (else the translated L differs from reduce's; the bbox is still checked)
+        assert pre["width"] == p
+        assert np.array_equal(pre["chain"], chain)
+        assert np.array_equal(pre["hull"], orc.melkman(chain))
